@@ -1,0 +1,393 @@
+// api.cu -- the C ABI of libtetproj (include/tetproj.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace tetproj;
+
+struct tet_mesh {
+    int device = 0;
+    uint32_t flags = 0;
+    HostMesh host;      // keeps grid parameters (arrays freed after upload)
+    DevMesh dev;
+    void* d_rec = nullptr;
+    void* d_vtx = nullptr;
+    void* d_hull = nullptr;
+    void* d_perm = nullptr;
+    int64_t bytes = 0;
+    // kernel timing (tet_set_kernel_timing)
+    struct TimerRec { int kind; cudaEvent_t a, b; };
+    std::mutex tmu;
+    bool timing = false;
+    std::vector<TimerRec> pending;
+    std::vector<cudaEvent_t> spare;
+    double ms[TET_K_COUNT] = {0, 0, 0, 0};
+    int64_t launches[TET_K_COUNT] = {0, 0, 0, 0};
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+tet_status fail(tet_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+tet_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(e == cudaErrorMemoryAllocation ? TET_E_NOMEM : TET_E_CUDA,
+                std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CU(call)                                             \
+    do {                                                     \
+        cudaError_t _e = (call);                             \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+    } while (0)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Is `p` device memory of `dev`?  (host pinned / pageable -> false)
+bool is_device_ptr(const void* p, int dev, bool& wrong_device) {
+    wrong_device = false;
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+        if (at.type == cudaMemoryTypeDevice && at.device != dev) wrong_device = true;
+        return true;
+    }
+    return false;
+}
+
+// Scratch allocated stream-ordered from the device's default pool.
+struct Scratch {
+    cudaStream_t s;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    cudaError_t alloc(void** p, size_t n) {
+        cudaError_t e = cudaMallocAsync(p, n ? n : 16, s);
+        if (e == cudaSuccess) ptrs.push_back(*p);
+        return e;
+    }
+    ~Scratch() {
+        for (void* p : ptrs) cudaFreeAsync(p, s);
+    }
+};
+
+void pool_setup(int dev) {
+    static bool done[64] = {false};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;  // keep freed scratch cached across calls
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
+enum class Op { Forward, Backward, BackwardF64 };
+
+cudaEvent_t take_event(tet_mesh* m) {
+    cudaEvent_t e = nullptr;
+    if (!m->spare.empty()) {
+        e = m->spare.back();
+        m->spare.pop_back();
+    } else {
+        cudaEventCreate(&e);
+    }
+    return e;
+}
+
+// Records CUDA events around one kernel launch when timing is enabled.
+struct KernelTimer {
+    tet_mesh* m;
+    int kind;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    KernelTimer(tet_mesh* mm, int k, cudaStream_t st) : m(mm), kind(k), s(st) {
+        if (!m->timing) return;
+        std::lock_guard<std::mutex> g(m->tmu);
+        a = take_event(m);
+        cudaEventRecord(a, s);
+    }
+    ~KernelTimer() {
+        if (!a) return;
+        std::lock_guard<std::mutex> g(m->tmu);
+        cudaEvent_t b = take_event(m);
+        cudaEventRecord(b, s);
+        m->pending.push_back({kind, a, b});
+    }
+};
+
+// Shared driver: geometry prep, chunking over angles, entry finder, walker.
+tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, int accumulate,
+               Op op, void* stream, tet_stats* st) {
+    if (!m) return fail(TET_E_ARG, "null mesh");
+    if (!g || !in || !out) return fail(TET_E_ARG, "null argument");
+    std::vector<AngleGeom> ang;
+    std::vector<AngleAux> aux;
+    std::string err;
+    tet_status rs = prepare_geometry(m->host, g, ang, aux, err);
+    if (rs != TET_OK) return fail(rs, err);
+    DeviceGuard guard(m->device);
+    pool_setup(m->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nrays = (int64_t)g->n_angles * g->n_v * g->n_u;
+    const int64_t nt = m->dev.nt;
+    bool wd_in = false, wd_out = false;
+    const bool dev_in = is_device_ptr(in, m->device, wd_in);
+    const bool dev_out = is_device_ptr(out, m->device, wd_out);
+    if (wd_in || wd_out) return fail(TET_E_ARG, "device pointer on another device than the mesh");
+    if (op == Op::BackwardF64 && !dev_out) return fail(TET_E_ARG, "tet_backproject_f64 needs a device accumulator");
+    const size_t in_bytes = (op == Op::Forward ? nt : nrays) * sizeof(float);
+    const size_t out_elems = (op == Op::Forward ? nrays : nt);
+    const bool strict = (m->flags & TET_F_STRICT) != 0;
+    const bool need_stats = st || strict;
+    unsigned long long hs[ST_COUNT] = {0};
+    {
+        Scratch sc(s);  // released (stream-ordered) at the end of this scope
+        // --- stage host inputs / outputs through device memory
+        const float* d_in = in;
+        if (!dev_in) {
+            void* p;
+            CU(sc.alloc(&p, in_bytes));
+            CU(cudaMemcpyAsync(p, in, in_bytes, cudaMemcpyHostToDevice, s));
+            d_in = (const float*)p;
+        }
+        void* d_out = out;
+        if (!dev_out) {
+            CU(sc.alloc(&d_out, out_elems * sizeof(float)));
+            if (op == Op::Backward && accumulate)
+                CU(cudaMemcpyAsync(d_out, out, out_elems * sizeof(float), cudaMemcpyHostToDevice, s));
+        }
+        // --- geometry tables
+        AngleGeom* d_ang;
+        AngleAux* d_aux;
+        unsigned long long* d_stats;
+        CU(sc.alloc((void**)&d_ang, sizeof(AngleGeom) * ang.size()));
+        CU(sc.alloc((void**)&d_aux, sizeof(AngleAux) * aux.size()));
+        CU(sc.alloc((void**)&d_stats, sizeof(unsigned long long) * ST_COUNT));
+        CU(cudaMemcpyAsync(d_ang, ang.data(), sizeof(AngleGeom) * ang.size(), cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(d_aux, aux.data(), sizeof(AngleAux) * aux.size(), cudaMemcpyHostToDevice, s));
+        CU(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * ST_COUNT, s));
+        // --- per-op buffers
+        float* mu_int = nullptr;
+        double* acc = nullptr;
+        if (op == Op::Forward) {
+            CU(sc.alloc((void**)&mu_int, nt * sizeof(float)));
+            KernelTimer kt(m, TET_K_PERMUTE, s);
+            CU(launch_gather_mu(m->dev, d_in, mu_int, s));
+        } else {
+            CU(sc.alloc((void**)&acc, nt * sizeof(double)));
+            CU(cudaMemsetAsync(acc, 0, nt * sizeof(double), s));
+        }
+        // --- angle chunks bound the entry-map scratch (<= 2^26 rays per chunk)
+        const int64_t per_angle = (int64_t)g->n_v * g->n_u;
+        const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(g->n_angles, (1LL << 26) / per_angle));
+        int* entry;
+        CU(sc.alloc((void**)&entry, sizeof(int) * per_angle * chunk));
+        for (int a0 = 0; a0 < g->n_angles; a0 += chunk) {
+            const int na = std::min(chunk, g->n_angles - a0);
+            LaunchChunk c{d_ang + a0, d_aux + a0, g->beam, na, g->n_v, g->n_u};
+            CU(cudaMemsetAsync(entry, 0xff, sizeof(int) * per_angle * na, s));
+            {
+                KernelTimer kt(m, TET_K_ENTRY, s);
+                CU(launch_entry(m->dev, c, entry, d_stats, s));
+            }
+            const size_t off = (size_t)a0 * per_angle;
+            if (op == Op::Forward) {
+                KernelTimer kt(m, TET_K_FORWARD, s);
+                CU(launch_forward(m->dev, c, entry, mu_int, (float*)d_out + off, d_stats, s));
+            } else {
+                KernelTimer kt(m, TET_K_BACKWARD, s);
+                CU(launch_backward(m->dev, c, entry, d_in + off, acc, d_stats, s));
+            }
+        }
+        if (op == Op::Backward) {
+            KernelTimer kt(m, TET_K_PERMUTE, s);
+            CU(launch_scatter_x(m->dev, acc, (float*)d_out, accumulate, s));
+        }
+        if (op == Op::BackwardF64) {
+            KernelTimer kt(m, TET_K_PERMUTE, s);
+            CU(launch_scatter_acc(m->dev, acc, (double*)d_out, s));
+        }
+        if (!dev_out)
+            CU(cudaMemcpyAsync(out, d_out, out_elems * sizeof(float), cudaMemcpyDeviceToHost, s));
+        if (need_stats) CU(cudaMemcpyAsync(hs, d_stats, sizeof hs, cudaMemcpyDeviceToHost, s));
+        CU(cudaGetLastError());
+    }
+    if (need_stats || !dev_out || !dev_in) CU(cudaStreamSynchronize(s));
+    if (st) {
+        std::memset(st, 0, sizeof *st);
+        st->rays = hs[ST_RAYS];
+        st->rays_hit = hs[ST_HIT];
+        st->crossings = hs[ST_CROSS];
+        st->lost = hs[ST_LOST];
+        st->stuck = hs[ST_STUCK];
+        st->exact_fallbacks = hs[ST_EXACT];
+        st->entry_conflicts = hs[ST_CONFLICT];
+        st->max_crossings_per_ray = (uint32_t)hs[ST_MAXC];
+    }
+    if (strict && (hs[ST_LOST] || hs[ST_STUCK] || hs[ST_CONFLICT]))
+        return fail(TET_E_RAYS, "lost / stuck / conflicting rays (TET_F_STRICT)");
+    return TET_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tet_last_error(void) { return g_err.c_str(); }
+
+tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* tets,
+                           const int32_t* nbrs, int64_t n_tets, const int32_t* bfaces,
+                           int64_t n_bfaces, int device, uint32_t flags, tet_mesh_t* out) {
+    if (!out) return fail(TET_E_ARG, "null output handle");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return fail(TET_E_CUDA, "no such CUDA device: " + std::to_string(device));
+    }
+    tet_mesh* m = new tet_mesh();
+    std::string err;
+    tet_status s = prepare_mesh(verts, n_verts, tets, nbrs, n_tets, bfaces, n_bfaces, flags,
+                                m->host, err);
+    if (s != TET_OK) {
+        delete m;
+        return fail(s, err);
+    }
+    m->device = device;
+    m->flags = flags;
+    DeviceGuard guard(device);
+    HostMesh& H = m->host;
+    auto up = [&](void** d, const void* h, size_t n) -> cudaError_t {
+        cudaError_t e = cudaMalloc(d, n ? n : 16);
+        if (e == cudaSuccess && n) e = cudaMemcpy(*d, h, n, cudaMemcpyHostToDevice);
+        m->bytes += (int64_t)n;
+        return e;
+    };
+    cudaError_t e = up(&m->d_rec, H.rec.data(), H.rec.size() * 4);
+    if (e == cudaSuccess) e = up(&m->d_vtx, H.vtx.data(), H.vtx.size() * 4);
+    if (e == cudaSuccess) e = up(&m->d_hull, H.hull.data(), H.hull.size() * 4);
+    if (e == cudaSuccess) e = up(&m->d_perm, H.perm.data(), H.perm.size() * 4);
+    if (e != cudaSuccess) {
+        tet_mesh_destroy(m);
+        return cuda_fail(e, "tet_mesh_create upload");
+    }
+    m->dev.rec = (const int4*)m->d_rec;
+    m->dev.vtx = (const int4*)m->d_vtx;
+    m->dev.hull = (const int2*)m->d_hull;
+    m->dev.perm = (const int*)m->d_perm;
+    m->dev.nv = H.nv;
+    m->dev.nt = H.nt;
+    m->dev.nb = H.nb;
+    m->dev.g = H.g;
+    m->dev.rmax = H.rmax;
+    // host copies are no longer needed
+    std::vector<int32_t>().swap(H.rec);
+    std::vector<int32_t>().swap(H.vtx);
+    std::vector<int32_t>().swap(H.hull);
+    std::vector<int32_t>().swap(H.perm);
+    *out = m;
+    return TET_OK;
+}
+
+tet_status tet_mesh_destroy(tet_mesh_t m) {
+    if (!m) return TET_OK;
+    DeviceGuard guard(m->device);
+    for (auto& r : m->pending) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : m->spare) cudaEventDestroy(e);
+    cudaFree(m->d_rec);
+    cudaFree(m->d_vtx);
+    cudaFree(m->d_hull);
+    cudaFree(m->d_perm);
+    delete m;
+    return TET_OK;
+}
+
+tet_status tet_project(tet_mesh_t m, const tet_geometry* g, const float* mu, float* proj,
+                       void* cuda_stream, tet_stats* st) {
+    return run(m, g, mu, proj, 0, Op::Forward, cuda_stream, st);
+}
+
+tet_status tet_backproject(tet_mesh_t m, const tet_geometry* g, const float* proj, float* x,
+                           int accumulate, void* cuda_stream, tet_stats* st) {
+    return run(m, g, proj, x, accumulate, Op::Backward, cuda_stream, st);
+}
+
+tet_status tet_backproject_f64(tet_mesh_t m, const tet_geometry* g, const float* proj,
+                               double* acc, void* cuda_stream, tet_stats* st) {
+    return run(m, g, proj, acc, 1, Op::BackwardF64, cuda_stream, st);
+}
+
+tet_status tet_set_kernel_timing(tet_mesh_t m, int enable) {
+    if (!m) return fail(TET_E_ARG, "null mesh");
+    std::lock_guard<std::mutex> g(m->tmu);
+    m->timing = enable != 0;
+    return TET_OK;
+}
+
+tet_status tet_kernel_times(tet_mesh_t m, double ms[4], int64_t launches[4]) {
+    if (!m || !ms || !launches) return fail(TET_E_ARG, "null argument");
+    DeviceGuard guard(m->device);
+    std::lock_guard<std::mutex> g(m->tmu);
+    for (auto& r : m->pending) {
+        float t = 0;
+        cudaError_t e = cudaEventElapsedTime(&t, r.a, r.b);
+        if (e != cudaSuccess) return cuda_fail(e, "tet_kernel_times (stream not synchronised?)");
+        m->ms[r.kind] += t;
+        m->launches[r.kind] += 1;
+        m->spare.push_back(r.a);
+        m->spare.push_back(r.b);
+    }
+    m->pending.clear();
+    for (int k = 0; k < TET_K_COUNT; ++k) {
+        ms[k] = m->ms[k];
+        launches[k] = m->launches[k];
+        m->ms[k] = 0;
+        m->launches[k] = 0;
+    }
+    return TET_OK;
+}
+
+tet_status tet_mesh_info(tet_mesh_t m, int64_t info[8]) {
+    if (!m || !info) return fail(TET_E_ARG, "null argument");
+    info[0] = m->dev.nv;
+    info[1] = m->dev.nt;
+    info[2] = m->dev.nb;
+    info[3] = m->device;
+    info[4] = m->host.e;
+    info[5] = m->bytes;
+    info[6] = 0;
+    info[7] = m->host.reordered ? 1 : 0;
+    return TET_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// internal.h -- types shared by the host preparation, the kernels and the C ABI
+// of libtetproj (product path; independent of oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/tetproj.h"
+
+namespace tetproj {
+
+// Per-angle scan geometry on the integer grid.
+struct AngleGeom {
+    long long o[3];    // cone: source S; parallel: direction d (ray o = p - d)
+    long long p00[3];  // centre of pixel (v=0,u=0)
+    long long du[3];   // u step
+    long long dv[3];   // v step
+};
+
+// Per-angle doubles used only to bound the detector footprint of hull faces
+// (never for a crossing decision).
+struct AngleAux {
+    double S[3];      // cone source / parallel direction (grid units)
+    double P00[3];
+    double N[3];      // U x V
+    double Us[3];     // dual vector: u = (Q - P00) . Us
+    double Vs[3];     // dual vector: v = (Q - P00) . Vs
+};
+
+// Host-side prepared mesh (internal SFC order).
+struct HostMesh {
+    int64_t nv = 0, nt = 0, nb = 0;
+    int e = 0;                 // grid exponent, g = 2^e
+    double g = 0, C[3] = {0, 0, 0};
+    std::vector<int32_t> vtx;  // [V][4] grid coords (x,y,z,0), internal vertex order
+    std::vector<int32_t> rec;  // [T][8] nodes(4) | nbr tags(4): (n<<2 | k') or -1
+    std::vector<int32_t> hull; // [B][2] (t, k) internal order
+    std::vector<int32_t> perm; // [T] internal -> caller tet index
+    double rmax = 0;           // max |X|_2 over vertices (grid units)
+    double bs_c[3] = {0, 0, 0}, bs_r = 0;  // bounding sphere (grid units)
+    bool reordered = false;
+};
+
+// Prepare (validate, orient, snap, reorder, pack).  Returns TET_OK or an
+// error with text in `err`.
+tet_status prepare_mesh(const double* verts, int64_t nv, const int32_t* tets,
+                        const int32_t* nbrs, int64_t nt, const int32_t* bfaces,
+                        int64_t nb, uint32_t flags, HostMesh& out, std::string& err);
+
+// Snap a geometry to the mesh grid and validate it.
+tet_status prepare_geometry(const HostMesh& m, const tet_geometry* g,
+                            std::vector<AngleGeom>& ang, std::vector<AngleAux>& aux,
+                            std::string& err);
+
+// ------------------------------------------------------------- device ----
+struct DevMesh {
+    const int4* rec = nullptr;   // [2T]
+    const int4* vtx = nullptr;   // [V]
+    const int2* hull = nullptr;  // [B]
+    const int* perm = nullptr;   // [T]
+    int64_t nv = 0, nt = 0, nb = 0;
+    double g = 0, rmax = 0;
+};
+
+enum StatSlot {
+    ST_RAYS = 0, ST_HIT, ST_CROSS, ST_LOST, ST_STUCK, ST_EXACT, ST_CONFLICT, ST_MAXC,
+    ST_COUNT
+};
+
+struct LaunchChunk {
+    const AngleGeom* ang;   // device, chunk-local angles
+    const AngleAux* aux;    // device
+    int beam, n_angles, nv, nu;
+};
+
+// kernel launchers (kernels.cu)
+cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry,
+                         unsigned long long* stats, cudaStream_t s);
+cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
+                           const float* mu_int, float* proj, unsigned long long* stats,
+                           cudaStream_t s);
+cudaError_t launch_backward(const DevMesh& m, const LaunchChunk& c, const int* entry,
+                            const float* y, double* acc, unsigned long long* stats,
+                            cudaStream_t s);
+cudaError_t launch_gather_mu(const DevMesh& m, const float* mu, float* mu_int,
+                             cudaStream_t s);
+cudaError_t launch_scatter_x(const DevMesh& m, const double* acc, float* x, int accumulate,
+                             cudaStream_t s);
+cudaError_t launch_scatter_acc(const DevMesh& m, const double* acc, double* out,
+                               cudaStream_t s);
+
+}  // namespace tetproj

@@ -1,0 +1,263 @@
+"""Thin ctypes binding of libtetproj (include/tetproj.h) -- argument
+marshalling only; every step of the path runs in the CUDA library.
+
+Names mirror the C ABI: ``tet_mesh_create``, ``tet_project``,
+``tet_backproject``, ``tet_backproject_f64``, ``tet_mesh_info``,
+``tet_mesh_destroy``.  Data arguments may be torch CUDA tensors (device
+pointers, asynchronous on the current torch stream) or numpy arrays / torch
+CPU tensors (host pointers; the library stages them through the device).
+
+There is no CPU fallback: if ``libtetproj.so`` is missing or no CUDA device
+is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _build
+
+TET_OK, TET_E_ARG, TET_E_MESH, TET_E_NONCONVEX, TET_E_GEOMETRY, TET_E_CUDA, TET_E_NOMEM, \
+    TET_E_RAYS = range(8)
+TET_BEAM_CONE, TET_BEAM_PARALLEL = 0, 1
+TET_F_FIX_ORIENTATION, TET_F_NO_REORDER, TET_F_STRICT = 1, 2, 4
+_STATUS = ["TET_OK", "TET_E_ARG", "TET_E_MESH", "TET_E_NONCONVEX", "TET_E_GEOMETRY",
+           "TET_E_CUDA", "TET_E_NOMEM", "TET_E_RAYS"]
+
+
+class TetProjError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        name = _STATUS[status] if 0 <= status < len(_STATUS) else str(status)
+        super().__init__(f"{name}: {msg}")
+        self.status = status
+
+
+class tet_geometry(C.Structure):
+    _fields_ = [("beam", C.c_int32), ("n_angles", C.c_int32), ("n_v", C.c_int32),
+                ("n_u", C.c_int32), ("vecs", C.POINTER(C.c_double))]
+
+
+class tet_stats(C.Structure):
+    _fields_ = [("rays", C.c_uint64), ("rays_hit", C.c_uint64), ("crossings", C.c_uint64),
+                ("lost", C.c_uint64), ("stuck", C.c_uint64), ("exact_fallbacks", C.c_uint64),
+                ("entry_conflicts", C.c_uint64), ("max_crossings_per_ray", C.c_uint32),
+                ("_pad", C.c_uint32)]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_ if k != "_pad"}
+
+
+EXPORTS = ["tet_mesh_create", "tet_mesh_destroy", "tet_project", "tet_backproject",
+           "tet_backproject_f64", "tet_mesh_info", "tet_last_error", "tet_set_kernel_timing",
+           "tet_kernel_times"]
+KERNEL_CLASSES = ["entry", "forward", "backward", "permute"]
+
+_lib = None
+
+
+def lib(build: bool = False) -> C.CDLL:
+    """Load libtetproj.so (in-tree).  Raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build:
+        _build.build()
+    if not os.path.exists(_build.LIB):
+        raise ImportError(f"{_build.LIB} not built: run `python -m paper_1908_06909_b200._build` "
+                          "or __graft_entry__.build()")
+    L = C.CDLL(_build.LIB)
+    P = C.c_void_p
+    L.tet_mesh_create.argtypes = [P, C.c_int64, P, P, C.c_int64, P, C.c_int64, C.c_int,
+                                  C.c_uint32, C.POINTER(C.c_void_p)]
+    L.tet_mesh_destroy.argtypes = [P]
+    L.tet_project.argtypes = [P, C.POINTER(tet_geometry), P, P, P, C.POINTER(tet_stats)]
+    L.tet_backproject.argtypes = [P, C.POINTER(tet_geometry), P, P, C.c_int, P,
+                                  C.POINTER(tet_stats)]
+    L.tet_backproject_f64.argtypes = [P, C.POINTER(tet_geometry), P, P, P,
+                                      C.POINTER(tet_stats)]
+    L.tet_mesh_info.argtypes = [P, C.POINTER(C.c_int64)]
+    L.tet_set_kernel_timing.argtypes = [P, C.c_int]
+    L.tet_kernel_times.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    L.tet_last_error.restype = C.c_char_p
+    for f in ("tet_mesh_create", "tet_mesh_destroy", "tet_project", "tet_backproject",
+              "tet_backproject_f64", "tet_mesh_info", "tet_set_kernel_timing",
+              "tet_kernel_times"):
+        getattr(L, f).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != TET_OK:
+        raise TetProjError(status, lib().tet_last_error().decode())
+
+
+def _host(a, dtype):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return a, a.ctypes.data_as(C.c_void_p)
+
+
+def _ptr(t, dtype, n):
+    """(keepalive, void*) for a torch tensor (device or host) or numpy array."""
+    try:
+        import torch
+        if isinstance(t, torch.Tensor):
+            want = {np.float32: torch.float32, np.float64: torch.float64}[dtype]
+            if t.dtype != want or not t.is_contiguous():
+                raise TypeError(f"expected a contiguous {want} tensor")
+            if t.numel() != n:
+                raise ValueError(f"expected {n} elements, got {t.numel()}")
+            return t, C.c_void_p(t.data_ptr())
+    except ImportError:
+        pass
+    if not isinstance(t, np.ndarray) or t.dtype != dtype or not t.flags.c_contiguous:
+        raise TypeError(f"expected a contiguous numpy {np.dtype(dtype).name} array")
+    if t.size != n:
+        raise ValueError(f"expected {n} elements, got {t.size}")
+    return t, t.ctypes.data_as(C.c_void_p)
+
+
+def _stream(stream, *tensors):
+    if stream is not None:
+        return C.c_void_p(int(stream))
+    try:
+        import torch
+        for t in tensors:
+            if isinstance(t, torch.Tensor) and t.is_cuda:
+                return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+    except ImportError:
+        pass
+    return C.c_void_p(0)
+
+
+def _geom(g):
+    vecs = np.ascontiguousarray(g.vecs, dtype=np.float64)
+    assert vecs.shape == (g.n_angles, 12)
+    s = tet_geometry(int(g.beam), int(g.n_angles), int(g.n_v), int(g.n_u),
+                     vecs.ctypes.data_as(C.POINTER(C.c_double)))
+    return s, vecs
+
+
+@dataclass
+class MeshHandle:
+    ptr: C.c_void_p
+    n_tets: int
+    n_verts: int
+    device: int
+
+    def __del__(self):
+        if self.ptr is not None and _lib is not None:
+            _lib.tet_mesh_destroy(self.ptr)
+            self.ptr = None
+
+
+def tet_mesh_create(verts, tets, nbrs, bfaces, device: int = 0,
+                    flags: int = TET_F_FIX_ORIENTATION) -> MeshHandle:
+    v, pv = _host(verts, np.float64)
+    t, pt = _host(tets, np.int32)
+    n, pn = _host(nbrs, np.int32)
+    b, pb = _host(bfaces, np.int32)
+    assert v.ndim == 2 and v.shape[1] == 3 and t.shape[1:] == (4,) and n.shape == t.shape
+    h = C.c_void_p()
+    _check(lib().tet_mesh_create(pv, v.shape[0], pt, pn, t.shape[0], pb, b.shape[0], device,
+                                 flags, C.byref(h)))
+    return MeshHandle(h, int(t.shape[0]), int(v.shape[0]), device)
+
+
+def tet_mesh_destroy(m: MeshHandle):
+    if m.ptr is not None:
+        _check(lib().tet_mesh_destroy(m.ptr))
+        m.ptr = None
+
+
+def tet_mesh_info(m: MeshHandle) -> dict:
+    info = (C.c_int64 * 8)()
+    _check(lib().tet_mesh_info(m.ptr, info))
+    keys = ["n_verts", "n_tets", "n_bfaces", "device", "grid_exponent", "device_bytes",
+            "l2_window_bytes", "reordered"]
+    return dict(zip(keys, [int(x) for x in info]))
+
+
+def tet_set_kernel_timing(m: MeshHandle, enable: bool = True):
+    _check(lib().tet_set_kernel_timing(m.ptr, 1 if enable else 0))
+
+
+def tet_kernel_times(m: MeshHandle) -> dict:
+    """{class: (ms, launches)} accumulated since the last read (stream synced)."""
+    ms = (C.c_double * 4)()
+    n = (C.c_int64 * 4)()
+    _check(lib().tet_kernel_times(m.ptr, ms, n))
+    return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(KERNEL_CLASSES)}
+
+
+def tet_project(m: MeshHandle, geom, mu, proj, stream=None, stats: bool = False):
+    """proj = A mu (Eq. 2).  Returns the stats dict when ``stats``."""
+    g, keep = _geom(geom)
+    _, pmu = _ptr(mu, np.float32, m.n_tets)
+    _, pp = _ptr(proj, np.float32, geom.n_angles * geom.n_v * geom.n_u)
+    st = tet_stats()
+    _check(lib().tet_project(m.ptr, C.byref(g), pmu, pp, _stream(stream, mu, proj),
+                             C.byref(st) if stats else None))
+    return st.as_dict() if stats else None
+
+
+def tet_backproject(m: MeshHandle, geom, proj, x, accumulate: bool = False, stream=None,
+                    stats: bool = False):
+    """x = A^T proj (Eq. 3), or x += A^T proj."""
+    g, keep = _geom(geom)
+    _, pp = _ptr(proj, np.float32, geom.n_angles * geom.n_v * geom.n_u)
+    _, px = _ptr(x, np.float32, m.n_tets)
+    st = tet_stats()
+    _check(lib().tet_backproject(m.ptr, C.byref(g), pp, px, 1 if accumulate else 0,
+                                 _stream(stream, proj, x), C.byref(st) if stats else None))
+    return st.as_dict() if stats else None
+
+
+def tet_backproject_f64(m: MeshHandle, geom, proj, acc, stream=None, stats: bool = False):
+    """acc += A^T proj into a double device accumulator (multi-GPU partial sums)."""
+    g, keep = _geom(geom)
+    _, pp = _ptr(proj, np.float32, geom.n_angles * geom.n_v * geom.n_u)
+    _, pa = _ptr(acc, np.float64, m.n_tets)
+    st = tet_stats()
+    _check(lib().tet_backproject_f64(m.ptr, C.byref(g), pp, pa, _stream(stream, proj, acc),
+                                     C.byref(st) if stats else None))
+    return st.as_dict() if stats else None
+
+
+class TetMesh:
+    """Convenience wrapper: a mesh resident on one GPU plus torch-facing ops."""
+
+    def __init__(self, verts, tets, nbrs, bfaces, device: int = 0,
+                 flags: int = TET_F_FIX_ORIENTATION):
+        self.handle = tet_mesh_create(verts, tets, nbrs, bfaces, device, flags)
+        self.device = device
+
+    @classmethod
+    def from_mesh(cls, mesh, device: int = 0, flags: int = TET_F_FIX_ORIENTATION):
+        return cls(mesh.verts, mesh.tets, mesh.nbrs, mesh.bfaces, device, flags)
+
+    @property
+    def n_tets(self) -> int:
+        return self.handle.n_tets
+
+    def info(self) -> dict:
+        return tet_mesh_info(self.handle)
+
+    def project(self, geom, mu, out=None, stats: bool = False):
+        import torch
+        if out is None:
+            out = torch.empty((geom.n_angles, geom.n_v, geom.n_u), dtype=torch.float32,
+                              device=mu.device if isinstance(mu, torch.Tensor) else "cpu")
+        st = tet_project(self.handle, geom, mu, out, stats=stats)
+        return (out, st) if stats else out
+
+    def backproject(self, geom, proj, out=None, accumulate=False, stats: bool = False):
+        import torch
+        if out is None:
+            out = torch.zeros(self.n_tets, dtype=torch.float32,
+                              device=proj.device if isinstance(proj, torch.Tensor) else "cpu")
+        st = tet_backproject(self.handle, geom, proj, out, accumulate, stats=stats)
+        return (out, st) if stats else out

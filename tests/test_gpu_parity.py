@@ -1,0 +1,174 @@
+"""CUDA path vs the CPU oracle, element by element (GPU only).
+
+Tolerances (BASELINE.json north_star): forward <= 1e-4 relative per pixel,
+backprojection <= 1e-4 relative per tet, adjoint <= 1e-5, zero lost/stuck
+rays, and -- since both sides take the same exact combinatorial decisions --
+identical crossing counts.
+"""
+import numpy as np
+import pytest
+
+from tests import gpu_util as U
+from workloads import configs as CF
+from workloads import geometry as G
+from workloads import meshes as M
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_1908_06909_b200 import tetproj
+    tetproj.lib()
+
+
+def test_c1_full():
+    w = CF.workload("c1")
+    r = U.check_parity(w.mesh, w.geom, w.mu, w.y, expect_exact_fallbacks=True)
+    assert r["stats"]["rays_hit"] == 64
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_small_lattice_degenerate(seed):
+    m = M.random_small_mesh(25 + 5 * seed, seed)
+    geom = G.lattice_parallel((1 / 8,) * 3, (0, 0, 0), 19, 13, G.LATTICE_DIRS[seed::3][:5])
+    rng = np.random.default_rng(seed)
+    mu = rng.uniform(0.5, 1.5, m.n_tets).astype(np.float32)
+    y = rng.uniform(0.5, 1.5, geom.n_rays).astype(np.float32)
+    U.check_parity(m, geom, mu, y, expect_exact_fallbacks=True)
+
+
+def test_small_cone_through_vertices():
+    m = M.random_small_mesh(40, 5)
+    rows = []
+    for th in (0.0, 1.0, 2.5, 4.0):
+        S = np.round(np.array([4 * np.sin(th), -4 * np.cos(th), 0.25]) * 16) / 16
+        Uv = np.array([0.0625, 0, 0]) if abs(np.cos(th)) > 0.5 else np.array([0, 0.0625, 0])
+        V = np.array([0, 0, 0.0625])
+        rows.append(np.concatenate([S, -S - 20 * Uv - 17 * V, Uv, V]))
+    geom = G.explicit(G.BEAM_CONE, 35, 41, rows)
+    rng = np.random.default_rng(0)
+    mu = rng.uniform(0.5, 1.5, m.n_tets).astype(np.float32)
+    y = rng.uniform(0.5, 1.5, geom.n_rays).astype(np.float32)
+    U.check_parity(m, geom, mu, y)
+
+
+def test_c2_ball_ragged():
+    w = CF.workload("c2", n_angles=3, n_u=67, n_v=53)
+    U.check_parity(w.mesh, w.geom, w.mu, w.y)
+    w2 = CF.workload("c2", n_angles=2, n_u=45, n_v=37, mu="uniform")
+    U.check_parity(w2.mesh, w2.geom, w2.mu, w2.y)
+
+
+def test_c3_graded_ragged():
+    w = CF.workload("c3", n_angles=3, n_u=61, n_v=47)
+    U.check_parity(w.mesh, w.geom, w.mu, w.y)
+
+
+def test_c4a_sliver_lattice():
+    w = CF.workload("c4a", n_angles=6, n_u=72, n_v=40)
+    r = U.check_parity(w.mesh, w.geom, w.mu, w.y, expect_exact_fallbacks=True)
+    assert r["stats"]["rays_hit"] > 0
+
+
+def test_c4b_jittered_slivers():
+    w = CF.workload("c4b", n_angles=2, n_u=48, n_v=40)
+    U.check_parity(w.mesh, w.geom, w.mu, w.y)
+
+
+def test_empty_detector_misses_mesh():
+    m = M.ball_mesh(h=0.3, seed=3)
+    geom = G.circular_cone([0.0], 4.0, 8.0, 8, 8, 0.1, 0.1, off_u=200.0)
+    mu = np.ones(m.n_tets, np.float32)
+    y = np.ones(geom.n_rays, np.float32)
+    p, x, st, st2, _ = U.run_gpu(m, geom, mu, y)
+    assert st["rays_hit"] == 0 and np.all(p == 0) and np.all(x == 0)
+
+
+def test_single_pixel_and_single_tet():
+    m = M.single_tet()
+    geom = G.explicit(G.BEAM_PARALLEL, 1, 1, [[1, 0, 0, 0, 0.25, 0.25, 1, 0, 0, 0, 1, 0]])
+    p, x, st, st2, _ = U.run_gpu(m, geom, np.array([2.0], np.float32), np.array([3.0], np.float32))
+    assert abs(p.ravel()[0] - 1.0) < 1e-6
+    assert abs(x[0] - 1.5) < 1e-6                   # chord 0.5 * y 3
+
+
+def test_host_pointers_and_accumulate():
+    import torch
+
+    from paper_1908_06909_b200 import tetproj as T
+    w = CF.workload("c2", n_angles=2, n_u=33, n_v=29)
+    tm = T.TetMesh.from_mesh(w.mesh)
+    p_dev = tm.project(w.geom, torch.from_numpy(w.mu).cuda())
+    p_host = np.zeros((w.geom.n_angles, w.geom.n_v, w.geom.n_u), np.float32)
+    T.tet_project(tm.handle, w.geom, w.mu, p_host)
+    np.testing.assert_array_equal(p_dev.cpu().numpy(), p_host)
+    x_host = np.zeros(w.mesh.n_tets, np.float32)
+    T.tet_backproject(tm.handle, w.geom, w.y, x_host)
+    x2 = x_host.copy()
+    T.tet_backproject(tm.handle, w.geom, w.y, x2, accumulate=True)
+    np.testing.assert_allclose(x2, 2 * x_host, rtol=1e-6)
+    acc = torch.zeros(w.mesh.n_tets, dtype=torch.float64, device="cuda")
+    T.tet_backproject_f64(tm.handle, w.geom, torch.from_numpy(w.y.ravel()).cuda(), acc)
+    np.testing.assert_allclose(acc.cpu().numpy().astype(np.float32), x_host, rtol=1e-6)
+
+
+def test_no_reorder_flag_same_result():
+    from paper_1908_06909_b200 import tetproj as T
+    w = CF.workload("c2", n_angles=2, n_u=31, n_v=27)
+    a, xa, *_ = U.run_gpu(w.mesh, w.geom, w.mu, w.y)
+    b, xb, *_ = U.run_gpu(w.mesh, w.geom, w.mu, w.y,
+                          flags=T.TET_F_FIX_ORIENTATION | T.TET_F_NO_REORDER)
+    np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(xa, xb, rtol=1e-6, atol=1e-7)
+
+
+def test_errors_are_statuses():
+    from paper_1908_06909_b200 import tetproj as T
+    m = M.kuhn_cube()
+    bad = m.nbrs.copy()
+    bad[0, 0] = 5 if bad[0, 0] != 5 else 4
+    with pytest.raises(T.TetProjError) as e:
+        T.tet_mesh_create(m.verts, m.tets, bad, m.bfaces)
+    assert e.value.status == T.TET_E_MESH
+    a = M.kuhn_lattice(2)
+    keep = [i for i in range(a.n_tets) if i % 7 != 3]
+    nb, bf = M.build_graph(a.tets[keep])
+    with pytest.raises(T.TetProjError) as e:
+        T.tet_mesh_create(a.verts, a.tets[keep], nb, bf)
+    assert e.value.status in (T.TET_E_NONCONVEX, T.TET_E_MESH)
+    tm = T.TetMesh.from_mesh(M.ball_mesh(h=0.3, seed=3))
+    g_inside = G.circular_cone([0.0], 0.5, 8.0, 8, 8, 0.1, 0.1)   # source inside the mesh
+    with pytest.raises(T.TetProjError) as e:
+        tm.project(g_inside, np.ones(tm.n_tets, np.float32))
+    assert e.value.status == T.TET_E_GEOMETRY
+
+
+def test_full_size_c3_sampled():
+    """BASELINE config c3 at full size, in bench.py's launch configuration:
+    sampled rays vs the oracle one by one; backprojection via the adjoint and
+    the total-sum identity sum_t (A^T 1)_t = sum_j (A 1)_j."""
+    import torch
+
+    from oracle import tetref as O
+    w = CF.workload("c3")
+    p, x, st, st2, tm = U.run_gpu(w.mesh, w.geom, w.mu, w.y)
+    assert st["lost"] == st["stuck"] == st["entry_conflicts"] == 0
+    assert st2["lost"] == st2["stuck"] == 0
+    rng = np.random.default_rng(7)
+    ids = np.sort(rng.choice(w.geom.n_rays, 3000, replace=False))
+    om = O.OracleMesh.from_mesh(w.mesh)
+    pr, _ = O.project(om, w.geom, w.mu.astype(np.float64), ray_ids=ids)
+    fe = U.fwd_errors(p.ravel()[ids].astype(np.float64), pr, w.mu, w.mesh)
+    assert fe.max() <= U.FWD_TOL
+    lhs = float(np.dot(p.astype(np.float64).ravel(), w.y.astype(np.float64).ravel()))
+    rhs = float(np.dot(w.mu.astype(np.float64), x.astype(np.float64)))
+    assert abs(lhs - rhs) / abs(lhs) <= U.ADJ_TOL
+    ones_t = torch.ones(w.mesh.n_tets, device="cuda")
+    ones_r = torch.ones(w.geom.n_rays, device="cuda")
+    rowsum = tm.project(w.geom, ones_t).double().sum().item()
+    colsum = tm.backproject(w.geom, ones_r).double().sum().item()
+    assert abs(rowsum - colsum) / rowsum <= U.ADJ_TOL
