@@ -278,7 +278,7 @@ def main():
     proj_h = torch.empty(proj.shape, dtype=torch.float32).pin_memory()
     x_h = torch.empty(x.shape, dtype=torch.float32).pin_memory()
     e2e_ms = []
-    for i in range(args.e2e_steps + 1):
+    for i in range(args.e2e_steps + 1 if args.e2e_steps > 0 else 0):
         flush.zero_()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -293,10 +293,10 @@ def main():
         torch.cuda.synchronize()
         if i > 0:
             e2e_ms.append(a.elapsed_time(b))
-    e2e_t = torch.tensor([sum(e2e_ms) / 1e3], dtype=torch.float64, device=dev)
+    e2e_t = torch.tensor([max(sum(e2e_ms), 1e-9) / 1e3], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = (cf_all + cb_all) * len(e2e_ms) / e2e_t.item()
+    e2e_value = (cf_all + cb_all) * len(e2e_ms) / e2e_t.item() if e2e_ms else None
 
     if rank == 0:
         peak, peak_src = measured_peaks()

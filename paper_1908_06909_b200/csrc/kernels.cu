@@ -145,7 +145,8 @@ __device__ __forceinline__ void add_stat(unsigned long long* st, int slot, unsig
 // ------------------------------------------------------- entry finder ----
 // Direct det[A,B,D] (A=a-o, B=b-o, D=p-o exactly representable) with a
 // Shewchuk-style static bound; exact SoS when inside the bound.
-__device__ __forceinline__ int side_direct(const int4 a, const int4 b, const RayPts& r) {
+__device__ __forceinline__ int side_direct(const int4 a, const int4 b, const RayPts& r,
+                                           unsigned& n_exact) {
     const double Ax = (double)(a.x - r.ox), Ay = (double)(a.y - r.oy), Az = (double)(a.z - r.oz);
     const double Bx = (double)(b.x - r.ox), By = (double)(b.y - r.oy), Bz = (double)(b.z - r.oz);
     const double Dx = (double)(r.px - r.ox), Dy = (double)(r.py - r.oy), Dz = (double)(r.pz - r.oz);
@@ -157,8 +158,8 @@ __device__ __forceinline__ int side_direct(const int4 a, const int4 b, const Ray
     const double bound = perm * 0x1p-48;
     if (det > bound) return 1;
     if (det < -bound) return -1;
-    return sos_side(a.x, a.y, a.z, b.x, b.y, b.z, r.ox, r.oy, r.oz, r.px, r.py, r.pz) |
-           0x100;  // flag: exact path used
+    ++n_exact;
+    return sos_side(a.x, a.y, a.z, b.x, b.y, b.z, r.ox, r.oy, r.oz, r.px, r.py, r.pz);
 }
 
 __global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ rec,
@@ -240,15 +241,9 @@ __global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ rec
         const int u = u0 + (int)(i % bw), v = v0 + (int)(i / bw);
         const RayPts r = ray_points(G, beam, u, v);
         // entering iff side(a,b) = side(b,c) = side(c,a) = -1 (outward order)
-        int s = side_direct(A, B, r);
-        exact += s >> 8;
-        if ((s & 0xff) != 0xff) continue;  // (-1 & 0xff) == 0xff
-        s = side_direct(B, C, r);
-        exact += s >> 8;
-        if ((s & 0xff) != 0xff) continue;
-        s = side_direct(C, A, r);
-        exact += s >> 8;
-        if ((s & 0xff) != 0xff) continue;
+        if (side_direct(A, B, r, exact) != -1) continue;
+        if (side_direct(B, C, r, exact) != -1) continue;
+        if (side_direct(C, A, r, exact) != -1) continue;
         const int old = atomicExch(entry + ((size_t)a * nv + v) * nu + u, code);
         conflicts += (old != -1);
     }
@@ -344,9 +339,11 @@ __global__ void __launch_bounds__(128) trace_kernel(const int4* __restrict__ rec
             const double sw = wP + wQ + wR;
             double zout;
             if (sw > 0.0) {
-                // relative offset in fp32 (|offset| ~ tet size)
-                const float dz = __fdividef((float)wQ * (float)(zq - z3) + (float)wR * (float)(zr - z3), (float)sw);
-                zout = z3 + (double)dz;
+                // offset from the apex; 1/sw from the fp32 reciprocal refined by
+                // one fp64 Newton step (rel. error ~2^-46)
+                double rin = (double)__frcp_rn((float)sw);
+                rin = rin * fma(-sw, rin, 2.0);
+                zout = fma(fma(wQ, zq - z3, wR * (zr - z3)), rin, z3);
             } else {
                 zout = zin;
                 ++n_exact;

@@ -154,13 +154,13 @@ def _exact_orient_nonzero(verts_q: np.ndarray, tets: np.ndarray) -> np.ndarray:
     return ok
 
 
-def delaunay_mesh(points: np.ndarray, name: str, extra=None) -> Mesh:
+def delaunay_mesh(points: np.ndarray, name: str, extra=None, quant: float = QUANT) -> Mesh:
     from scipy.spatial import Delaunay
 
-    pts = np.unique(_quantize(np.asarray(points, dtype=np.float64)), axis=0)
+    pts = np.unique(np.round(np.asarray(points, dtype=np.float64) * quant) / quant, axis=0)
     tri = Delaunay(pts)
     tets = tri.simplices.astype(np.int64)
-    ok = _exact_orient_nonzero(np.round(pts * QUANT).astype(np.int64), tets)
+    ok = _exact_orient_nonzero(np.round(pts * quant).astype(np.int64), tets)
     if not ok.all():
         raise RuntimeError(f"{name}: Qhull produced {int((~ok).sum())} flat tets")
     # the neighbour table from Qhull uses the same opposite-vertex convention,
@@ -259,14 +259,20 @@ def jittered_lattice_mesh(n: int = 55, jitter: float = 1e-4, seed: int = 5) -> M
     """Config c4b: Delaunay of an (n+1)^3 lattice on [-1,1]^3 whose points are
     jittered by jitter*h (boundary points only in-plane) -> classic slivers
     (PAPER.md:325 "high aspect ratios")."""
-    rng = np.random.default_rng(seed)
     h = 2.0 / n
-    g = np.linspace(-1, 1, n + 1)
+    g = np.linspace(-1 + 2 * jitter * h, 1 - 2 * jitter * h, n + 1)  # jittered points stay in [-1,1]
     P = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
-    J = rng.uniform(-1, 1, P.shape) * jitter * h
-    J[np.isclose(np.abs(P), 1.0)] = 0.0   # keep boundary coordinates exact
-    P = P + J
-    return delaunay_mesh(P, f"jlattice_n{n}_j{jitter}_s{seed}")
+    for attempt in range(8):
+        # jitter in all directions (the hull is the convex hull of the jittered
+        # boundary points); quantise finely (2^-22) so coplanar quadruples,
+        # which make Qhull emit flat tets, are rare -- redraw if any appear.
+        rng = np.random.default_rng([seed, attempt])
+        J = rng.uniform(-1, 1, P.shape) * jitter * h
+        try:
+            return delaunay_mesh(P + J, f"jlattice_n{n}_j{jitter}_s{seed}", quant=2.0 ** 22)
+        except RuntimeError:
+            continue
+    raise RuntimeError("could not draw a jittered lattice without flat tets")
 
 
 def sliver_kuhn_mesh(n: int = 55) -> Mesh:
