@@ -81,43 +81,61 @@ __device__ __noinline__ int exact_side_ids(const int4* __restrict__ vtx,
 }
 
 // ------------------------------------------------------------ frame -----
+// Shear frame of a ray (the projection along the ray onto the coordinate
+// plane orthogonal to its dominant axis k):
+//     A = X - o,  x' = A_k1 - (D_k1/D_k) A_k,  y' = A_k2 - (D_k2/D_k) A_k,  z' = A_k
+// so that det[a-o, b-o, p-o] = D_k (x'_a y'_b - y'_a x'_b).  (k1,k2,k) is a
+// cyclic permutation of (x,y,z), with k1,k2 swapped when D_k < 0, which makes
+// side2() carry the sign of the determinant itself.  The computed side2() is
+// within ~26 eps Amax^2 of det/D_k (Amax >= |X - o| for every vertex), far
+// below tau = 2^-40 Amax^2.  z' of the crossing
+// points gives the chord: |D|/|D_k| * dz' * g.
 struct Frame {
-    double e1x, e1y, e1z, e2x, e2y, e2z, e3x, e3y, e3z;
-    double oe1, oe2, oe3;
-    double tau;
+    double sx, sy;         // D_k1/D_k, D_k2/D_k
+    double o1, o2, o3;     // o_k1, o_k2, o_k
+    double tau;            // sign-filter threshold
+    double scale;          // |D|/|D_k| * g
+    int k1, k2, k3;        // coordinate permutation
 };
 
-// Orthonormal frame with e3 = (p-o)/|p-o|; x,y of a point give
-// det[a-o,b-o,p-o]/|p-o| = x_a y_b - y_a x_b.  tau bounds the rounding error
-// of that 2x2 determinant for every vertex |X| <= rmax.
-__device__ __forceinline__ void make_frame(const RayPts& r, double rmax, Frame& F) {
-    const double Dx = (double)(r.px - r.ox), Dy = (double)(r.py - r.oy), Dz = (double)(r.pz - r.oz);
-    const double inv = rsqrt(Dx * Dx + Dy * Dy + Dz * Dz);
-    F.e3x = Dx * inv; F.e3y = Dy * inv; F.e3z = Dz * inv;
-    const double ax = fabs(F.e3x), ay = fabs(F.e3y), az = fabs(F.e3z);
-    double tx, ty, tz;
-    if (ax <= ay && ax <= az) { tx = 0.0; ty = F.e3z; tz = -F.e3y; }
-    else if (ay <= az)        { tx = -F.e3z; ty = 0.0; tz = F.e3x; }
-    else                      { tx = F.e3y; ty = -F.e3x; tz = 0.0; }
-    const double it = rsqrt(tx * tx + ty * ty + tz * tz);
-    F.e1x = tx * it; F.e1y = ty * it; F.e1z = tz * it;
-    F.e2x = F.e3y * F.e1z - F.e3z * F.e1y;
-    F.e2y = F.e3z * F.e1x - F.e3x * F.e1z;
-    F.e2z = F.e3x * F.e1y - F.e3y * F.e1x;
+__device__ __forceinline__ double comp(long long x, long long y, long long z, int k) {
+    return (double)(k == 0 ? x : (k == 1 ? y : z));
+}
+
+__device__ __forceinline__ void make_frame(const RayPts& r, double rmax, double g, Frame& F) {
+    const long long Dx = r.px - r.ox, Dy = r.py - r.oy, Dz = r.pz - r.oz;
+    const long long ax = Dx < 0 ? -Dx : Dx, ay = Dy < 0 ? -Dy : Dy, az = Dz < 0 ? -Dz : Dz;
+    int k = 2;
+    if (ax >= ay && ax >= az) k = 0;
+    else if (ay >= az) k = 1;
+    int k1 = k == 0 ? 1 : (k == 1 ? 2 : 0);
+    int k2 = k == 0 ? 2 : (k == 1 ? 0 : 1);
+    const double dk = comp(Dx, Dy, Dz, k);
+    if (dk < 0) { const int tmp = k1; k1 = k2; k2 = tmp; }
+    F.k1 = k1; F.k2 = k2; F.k3 = k;
+    F.sx = comp(Dx, Dy, Dz, k1) / dk;
+    F.sy = comp(Dx, Dy, Dz, k2) / dk;
+    F.o1 = comp(r.ox, r.oy, r.oz, k1);
+    F.o2 = comp(r.ox, r.oy, r.oz, k2);
+    F.o3 = comp(r.ox, r.oy, r.oz, k);
     const double ox = (double)r.ox, oy = (double)r.oy, oz = (double)r.oz;
-    F.oe1 = ox * F.e1x + oy * F.e1y + oz * F.e1z;
-    F.oe2 = ox * F.e2x + oy * F.e2y + oz * F.e2z;
-    F.oe3 = ox * F.e3x + oy * F.e3y + oz * F.e3z;
     const double amax = sqrt(ox * ox + oy * oy + oz * oz) + rmax;
     F.tau = amax * amax * 0x1p-40;
+    const double dx = (double)Dx, dy = (double)Dy, dz = (double)Dz;
+    F.scale = sqrt(dx * dx + dy * dy + dz * dz) / fabs(dk) * g;
+}
+
+__device__ __forceinline__ int icomp(const int4 v, int k) {
+    return k == 0 ? v.x : (k == 1 ? v.y : v.z);
 }
 
 __device__ __forceinline__ void xform(const Frame& F, const int4 v, double& x, double& y,
                                       double& z) {
-    const double X = (double)v.x, Y = (double)v.y, Z = (double)v.z;
-    x = fma(X, F.e1x, fma(Y, F.e1y, fma(Z, F.e1z, -F.oe1)));
-    y = fma(X, F.e2x, fma(Y, F.e2y, fma(Z, F.e2z, -F.oe2)));
-    z = fma(X, F.e3x, fma(Y, F.e3y, fma(Z, F.e3z, -F.oe3)));
+    const double a1 = (double)icomp(v, F.k1) - F.o1;   // exact (|.| < 2^33)
+    const double a2 = (double)icomp(v, F.k2) - F.o2;
+    z = (double)icomp(v, F.k3) - F.o3;
+    x = fma(-F.sx, z, a1);
+    y = fma(-F.sy, z, a2);
 }
 
 __device__ __forceinline__ double side2(double xa, double ya, double xb, double yb) {
@@ -252,6 +270,13 @@ __global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ rec
 }
 
 // ------------------------------------------------------------ walker ----
+// Certified sign of a side value (filter, else exact int128 + SoS).
+#define SIGN_OF(val, id_other, out)                                                   \
+    do {                                                                            \
+        out = (val) > F.tau ? 1 : ((val) < -F.tau ? -1 : 0);                        \
+        if (!out) { out = exact_side_ids(vtx, ang, beam, a, u, v, iap, id_other); ++n_exact; } \
+    } while (0)
+
 template <bool BACK>
 __global__ void __launch_bounds__(128) trace_kernel(const int4* __restrict__ rec,
                                                     const int4* __restrict__ vtx,
@@ -278,29 +303,29 @@ __global__ void __launch_bounds__(128) trace_kernel(const int4* __restrict__ rec
     unsigned n_cross = 0, n_exact = 0, n_lost = 0, n_stuck = 0;
     double sum = 0.0;
     if (e >= 0) {
-        const AngleGeom G = ang[a];
-        const RayPts r = ray_points(G, beam, u, v);
+        const RayPts r = ray_points(ang[a], beam, u, v);
         Frame F;
-        make_frame(r, rmax, F);
+        make_frame(r, rmax, g, F);
         const float yv = BACK ? y[rid] : 0.f;
         int t = e >> 2, kin = e & 3;
         int4 nodes = ldg_nc_v4(rec + 2 * (size_t)t);
-        int ia, ib, ic;
-        if (kin == 0)      { ia = nodes.y; ib = nodes.z; ic = nodes.w; }
-        else if (kin == 1) { ia = nodes.x; ib = nodes.w; ic = nodes.z; }
-        else if (kin == 2) { ia = nodes.x; ib = nodes.y; ic = nodes.w; }
-        else               { ia = nodes.x; ib = nodes.z; ic = nodes.y; }
-        double xa, ya, za, xb, yb, zb, xc, yc, zc;
-        xform(F, __ldg(vtx + ia), xa, ya, za);
-        xform(F, __ldg(vtx + ib), xb, yb, zb);
-        xform(F, __ldg(vtx + ic), xc, yc, zc);
-        // entry face sides (exact signs are all -1: certified by the entry finder)
-        double sab = side2(xa, ya, xb, yb), sbc = side2(xb, yb, xc, yc), sca = side2(xc, yc, xa, ya);
+        // three vertex slots holding the entry face in cyclic order; their edge
+        // sides s01, s12, s20 all have exact sign -1 (entering, R3)
+        int id0, id1, id2;
+        if (kin == 0)      { id0 = nodes.y; id1 = nodes.z; id2 = nodes.w; }
+        else if (kin == 1) { id0 = nodes.x; id1 = nodes.w; id2 = nodes.z; }
+        else if (kin == 2) { id0 = nodes.x; id1 = nodes.y; id2 = nodes.w; }
+        else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; }
+        double x0, y0, z0, x1, y1, z1, x2, y2, z2;
+        xform(F, __ldg(vtx + id0), x0, y0, z0);
+        xform(F, __ldg(vtx + id1), x1, y1, z1);
+        xform(F, __ldg(vtx + id2), x2, y2, z2);
+        double s01 = side2(x0, y0, x1, y1), s12 = side2(x1, y1, x2, y2), s20 = side2(x2, y2, x0, y0);
         double zin;
         {
-            const double wa = fmax(-sbc, 0.0), wb = fmax(-sca, 0.0), wc = fmax(-sab, 0.0);
-            const double sw = wa + wb + wc;
-            zin = sw > 0 ? (wa * za + wb * zb + wc * zc) / sw : (za + zb + zc) * (1.0 / 3.0);
+            const double w0 = fmax(-s12, 0.0), w1 = fmax(-s20, 0.0), w2 = fmax(-s01, 0.0);
+            const double sw = w0 + w1 + w2;
+            zin = sw > 0 ? (w0 * z0 + w1 * z1 + w2 * z2) / sw : (z0 + z1 + z2) * (1.0 / 3.0);
         }
         long long steps = 0;
         while (true) {
@@ -310,64 +335,68 @@ __global__ void __launch_bounds__(128) trace_kernel(const int4* __restrict__ rec
             const int iap = sel4(nodes, kin);  // apex: node opposite the entry face
             double x3, y3, z3;
             xform(F, __ldg(vtx + iap), x3, y3, z3);
-            const double pa = side2(x3, y3, xa, ya);
-            const double pb = side2(x3, y3, xb, yb);
-            const double pc = side2(x3, y3, xc, yc);
-            // exit: the unique i with sign(p_i) = -1 and sign(p_{i+1}) = +1
-            int sa = pa > F.tau ? 1 : pa < -F.tau ? -1 : 0;
-            if (!sa) { sa = exact_side_ids(vtx, ang, beam, a, u, v, iap, ia); ++n_exact; }
-            int i;
+            const double p0 = side2(x3, y3, x0, y0);   // side(apex, slot k)
+            const double p1 = side2(x3, y3, x1, y1);
+            const double p2 = side2(x3, y3, x2, y2);
+            // exit face (apex, slot i, slot i+1): the unique i with
+            // sign p_i = -1 and sign p_{i+1} = +1
+            int sa, sb, i;
+            SIGN_OF(p0, id0, sa);
             if (sa < 0) {
-                int sb = pb > F.tau ? 1 : pb < -F.tau ? -1 : 0;
-                if (!sb) { sb = exact_side_ids(vtx, ang, beam, a, u, v, iap, ib); ++n_exact; }
+                SIGN_OF(p1, id1, sb);
                 i = sb > 0 ? 0 : 1;
-                if (i == 1 && pc < -F.tau) ++n_lost;   // (-,-,-) is impossible
+                if (i == 1 && p2 < -F.tau) ++n_lost;   // (-,-,-) is impossible
             } else {
-                int sc = pc > F.tau ? 1 : pc < -F.tau ? -1 : 0;
-                if (!sc) { sc = exact_side_ids(vtx, ang, beam, a, u, v, iap, ic); ++n_exact; }
-                i = sc < 0 ? 2 : 1;
-                if (i == 1 && pb > F.tau) ++n_lost;    // (+,+,+) is impossible
+                SIGN_OF(p2, id2, sb);
+                i = sb < 0 ? 2 : 1;
+                if (i == 1 && p1 > F.tau) ++n_lost;    // (+,+,+) is impossible
             }
-            // exit face (apex, Q, R), opposite vertex O; weights of the crossing
-            // point: w_apex = -s(Q,R), w_Q = -s(R,apex) = p_R, w_R = -s(apex,Q) = -p_Q
-            int iq, ir, io;
-            double xq, yq, zq, xr, yr, zr, sqr, pq, pr;
-            if (i == 0)      { iq = ia; ir = ib; io = ic; xq = xa; yq = ya; zq = za; xr = xb; yr = yb; zr = zb; sqr = sab; pq = pa; pr = pb; }
-            else if (i == 1) { iq = ib; ir = ic; io = ia; xq = xb; yq = yb; zq = zb; xr = xc; yr = yc; zr = zc; sqr = sbc; pq = pb; pr = pc; }
-            else             { iq = ic; ir = ia; io = ib; xq = xc; yq = yc; zq = zc; xr = xa; yr = ya; zr = za; sqr = sca; pq = pc; pr = pa; }
-            const double wP = fmax(-sqr, 0.0), wQ = fmax(pr, 0.0), wR = fmax(-pq, 0.0);
-            const double sw = wP + wQ + wR;
+            const bool c0 = i == 0, c1 = i == 1;
+            // crossing point weights: apex -s(i,i+1), slot i p_{i+1}, slot i+1 -p_i
+            const double si = c0 ? s01 : (c1 ? s12 : s20);
+            const double pi = c0 ? p0 : (c1 ? p1 : p2);
+            const double pn = c0 ? p1 : (c1 ? p2 : p0);
+            const double zi = c0 ? z0 : (c1 ? z1 : z2);
+            const double zn = c0 ? z1 : (c1 ? z2 : z0);
+            const int idrop = c0 ? id2 : (c1 ? id0 : id1);  // slot i+2 leaves the face
+            const double wA = fmax(-si, 0.0), wQ = fmax(pn, 0.0), wR = fmax(-pi, 0.0);
+            const double sw = wA + wQ + wR;
             double zout;
             if (sw > 0.0) {
                 // offset from the apex; 1/sw from the fp32 reciprocal refined by
                 // one fp64 Newton step (rel. error ~2^-46)
                 double rin = (double)__frcp_rn((float)sw);
                 rin = rin * fma(-sw, rin, 2.0);
-                zout = fma(fma(wQ, zq - z3, wR * (zr - z3)), rin, z3);
+                zout = fma(fma(wQ, zi - z3, wR * (zn - z3)), rin, z3);
             } else {
                 zout = zin;
                 ++n_exact;
             }
-            const double chord = fmax(zout - zin, 0.0) * g;
+            const double chord = fmax(zout - zin, 0.0) * F.scale;
             if (BACK) {
                 if (chord > 0.0) atomicAdd(acc + t, chord * (double)yv);
             } else {
                 sum = fma(chord, (double)mut, sum);
             }
             ++n_cross;
-            // neighbour across the exit face = the face opposite O
-            const int lo = nodes.x == io ? 0 : nodes.y == io ? 1 : nodes.z == io ? 2 : 3;
+            // neighbour across the exit face = the face opposite the dropped vertex
+            const int lo = nodes.x == idrop ? 0 : nodes.y == idrop ? 1 : nodes.z == idrop ? 2 : 3;
             const int tag = sel4(tags, lo);
             if (tag < 0) break;
             if (++steps >= max_steps) { ++n_stuck; break; }
             t = tag >> 2;
             kin = tag & 3;
             nodes = ldg_nc_v4(rec + 2 * (size_t)t);
-            ia = iap; ib = iq; ic = ir;
-            xa = x3; ya = y3; za = z3;
-            xb = xq; yb = yq; zb = zq;
-            xc = xr; yc = yr; zc = zr;
-            sab = pq; sbc = sqr; sca = -pr;
+            // the apex takes the dropped slot i+2; cyclic order is preserved
+            const bool d0 = i == 1, d1 = i == 2, d2 = i == 0;
+            x0 = d0 ? x3 : x0; y0 = d0 ? y3 : y0; z0 = d0 ? z3 : z0; id0 = d0 ? iap : id0;
+            x1 = d1 ? x3 : x1; y1 = d1 ? y3 : y1; z1 = d1 ? z3 : z1; id1 = d1 ? iap : id1;
+            x2 = d2 ? x3 : x2; y2 = d2 ? y3 : y2; z2 = d2 ? z3 : z2; id2 = d2 ? iap : id2;
+            // s_{i+1} <- -p_{i+1}, s_{i+2} <- p_i
+            const double n01 = c1 ? p1 : (d1 ? -p0 : s01);
+            const double n12 = c0 ? -p1 : (d1 ? p2 : s12);
+            const double n20 = c0 ? p0 : (c1 ? -p2 : s20);
+            s01 = n01; s12 = n12; s20 = n20;
             zin = zout;
         }
     }
