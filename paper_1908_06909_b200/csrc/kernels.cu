@@ -89,12 +89,12 @@ __device__ __noinline__ int exact_side_ids(const int4* __restrict__ vtx,
 // side2() carry the sign of the determinant itself.  The computed side2() is
 // within ~26 eps Amax^2 of det/D_k (Amax >= |X - o| for every vertex), far
 // below tau = 2^-40 Amax^2.  z' of the crossing
-// points gives the chord: |D|/|D_k| * dz' * g.
+// points gives the chord: |D|/D_k * dz' * g.
 struct Frame {
     double sx, sy;         // D_k1/D_k, D_k2/D_k
     double o1, o2, o3;     // o_k1, o_k2, o_k
     double tau;            // sign-filter threshold
-    double scale;          // |D|/|D_k| * g
+    double scale;          // |D|/D_k * g (signed: z' decreases along the ray if D_k < 0)
     int k1, k2, k3;        // coordinate permutation
 };
 
@@ -122,7 +122,7 @@ __device__ __forceinline__ void make_frame(const RayPts& r, double rmax, double 
     const double amax = sqrt(ox * ox + oy * oy + oz * oz) + rmax;
     F.tau = amax * amax * 0x1p-40;
     const double dx = (double)Dx, dy = (double)Dy, dz = (double)Dz;
-    F.scale = sqrt(dx * dx + dy * dy + dz * dz) / fabs(dk) * g;
+    F.scale = sqrt(dx * dx + dy * dy + dz * dz) / dk * g;
 }
 
 __device__ __forceinline__ int icomp(const int4 v, int k) {
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(128) trace_kernel(const int4* __restrict__ rec
                 zout = zin;
                 ++n_exact;
             }
-            const double chord = fmax(zout - zin, 0.0) * F.scale;
+            const double chord = fmax((zout - zin) * F.scale, 0.0);
             if (BACK) {
                 if (chord > 0.0) atomicAdd(acc + t, chord * (double)yv);
             } else {
