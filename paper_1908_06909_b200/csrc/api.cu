@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -110,6 +111,25 @@ void pool_setup(int dev) {
 
 enum class Op { Forward, Backward, BackwardF64 };
 
+// Walker selection (benchmarking knob): TETPROJ_WALK=tiled uses one thread per
+// pixel (trace_kernel); default is the persistent refill walker.
+int walker_mode() {
+    static int mode = [] {
+        const char* e = std::getenv("TETPROJ_WALK");
+        return (e && std::strcmp(e, "tiled") == 0) ? 1 : 0;
+    }();
+    return mode;
+}
+
+int refill_threshold() {
+    static int r = [] {
+        const char* e = std::getenv("TETPROJ_REFILL");
+        int v = e ? std::atoi(e) : 16;
+        return v < 1 ? 1 : (v > 32 ? 32 : v);
+    }();
+    return r;
+}
+
 cudaEvent_t take_event(tet_mesh* m) {
     cudaEvent_t e = nullptr;
     if (!m->spare.empty()) {
@@ -209,6 +229,13 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(g->n_angles, (1LL << 26) / per_angle));
         int* entry;
         CU(sc.alloc((void**)&entry, sizeof(int) * per_angle * chunk));
+        const bool persistent = walker_mode() == 0;
+        int2* list = nullptr;
+        unsigned* counters = nullptr;  // [0] hit-list length, [1] walker fetch cursor
+        if (persistent) {
+            CU(sc.alloc((void**)&list, sizeof(int2) * per_angle * chunk));
+            CU(sc.alloc((void**)&counters, 2 * sizeof(unsigned)));
+        }
         for (int a0 = 0; a0 < g->n_angles; a0 += chunk) {
             const int na = std::min(chunk, g->n_angles - a0);
             LaunchChunk c{d_ang + a0, d_aux + a0, g->beam, na, g->n_v, g->n_u};
@@ -218,7 +245,18 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
                 CU(launch_entry(m->dev, c, entry, d_stats, s));
             }
             const size_t off = (size_t)a0 * per_angle;
-            if (op == Op::Forward) {
+            const bool fwd = op == Op::Forward;
+            if (persistent) {
+                CU(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned), s));
+                {
+                    KernelTimer kt(m, TET_K_ENTRY, s);
+                    CU(launch_hitlist(c, entry, list, counters, fwd ? (float*)d_out + off : nullptr, s));
+                }
+                KernelTimer kt(m, fwd ? TET_K_FORWARD : TET_K_BACKWARD, s);
+                CU(launch_walk(m->dev, c, !fwd, list, counters, counters + 1, refill_threshold(),
+                               mu_int, fwd ? (float*)d_out + off : nullptr, fwd ? nullptr : d_in + off,
+                               acc, d_stats, s));
+            } else if (fwd) {
                 KernelTimer kt(m, TET_K_FORWARD, s);
                 CU(launch_forward(m->dev, c, entry, mu_int, (float*)d_out + off, d_stats, s));
             } else {
@@ -242,7 +280,7 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
     if (need_stats || !dev_out || !dev_in) CU(cudaStreamSynchronize(s));
     if (st) {
         std::memset(st, 0, sizeof *st);
-        st->rays = hs[ST_RAYS];
+        st->rays = (uint64_t)nrays;
         st->rays_hit = hs[ST_HIT];
         st->crossings = hs[ST_CROSS];
         st->lost = hs[ST_LOST];

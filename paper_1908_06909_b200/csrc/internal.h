@@ -84,6 +84,12 @@ cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* en
 cudaError_t launch_backward(const DevMesh& m, const LaunchChunk& c, const int* entry,
                             const float* y, double* acc, unsigned long long* stats,
                             cudaStream_t s);
+cudaError_t launch_hitlist(const LaunchChunk& c, const int* entry, int2* list, unsigned* count,
+                           float* proj, cudaStream_t s);
+cudaError_t launch_walk(const DevMesh& m, const LaunchChunk& c, bool back, const int2* list,
+                        const unsigned* count, unsigned* next, int refill, const float* mu_int,
+                        float* proj, const float* y, double* acc, unsigned long long* stats,
+                        cudaStream_t s);
 cudaError_t launch_gather_mu(const DevMesh& m, const float* mu, float* mu_int,
                              cudaStream_t s);
 cudaError_t launch_scatter_x(const DevMesh& m, const double* acc, float* x, int accumulate,
