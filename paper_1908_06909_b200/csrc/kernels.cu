@@ -125,8 +125,23 @@ __device__ __forceinline__ void make_frame(const RayPts& r, double rmax, double 
     F.scale = sqrt(dx * dx + dy * dy + dz * dz) / dk * g;
 }
 
+// Branch-free selects (the ternary chains compiled to divergent branches).
+__device__ __forceinline__ int selp(int a, int b, bool p) {
+    int r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\tselp.b32 %0, %1, %2, q;\n\t}"
+        : "=r"(r) : "r"(a), "r"(b), "r"((int)p));
+    return r;
+}
+
 __device__ __forceinline__ int icomp(const int4 v, int k) {
-    return k == 0 ? v.x : (k == 1 ? v.y : v.z);
+    return selp(v.x, selp(v.y, v.z, k == 1), k == 0);
+}
+
+// reciprocal: MUFU approximation (~2^-23) + one fp64 Newton step (~2^-46)
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    return r * fma(-x, r, 2.0);
 }
 
 __device__ __forceinline__ void xform(const Frame& F, const int4 v, double& x, double& y,
@@ -143,7 +158,7 @@ __device__ __forceinline__ double side2(double xa, double ya, double xb, double 
 }
 
 __device__ __forceinline__ int sel4(int4 v, int k) {
-    return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+    return selp(selp(v.x, v.y, k == 0), selp(v.z, v.w, k == 2), k < 2);
 }
 
 __device__ __forceinline__ int4 ldg_nc_v4(const int4* p) {
@@ -278,7 +293,7 @@ __global__ void __launch_bounds__(128) trace_kernel(const int4* __restrict__ rec
                                                     const int4* __restrict__ vtx,
                                                     const AngleGeom* __restrict__ ang, int beam,
                                                     int nv, int nu, double rmax, double g,
-                                                    long long max_steps,
+                                                    int max_steps,
                                                     const int* __restrict__ entry,
                                                     const float* __restrict__ mu,
                                                     float* __restrict__ proj,
@@ -319,11 +334,11 @@ __global__ void __launch_bounds__(128) trace_kernel(const int4* __restrict__ rec
         double s01 = side2(x0, y0, x1, y1), s12 = side2(x1, y1, x2, y2), s20 = side2(x2, y2, x0, y0);
         double zin;
         {
-            const double w0 = fmax(-s12, 0.0), w1 = fmax(-s20, 0.0), w2 = fmax(-s01, 0.0);
+            const double w0 = fabs(s12), w1 = fabs(s20), w2 = fabs(s01);
             const double sw = w0 + w1 + w2;
             zin = sw > 0 ? (w0 * z0 + w1 * z1 + w2 * z2) / sw : (z0 + z1 + z2) * (1.0 / 3.0);
         }
-        long long steps = 0;
+        int steps = 0;
         while (true) {
             const int4 tags = ldg_nc_v4(rec + 2 * (size_t)t + 1);
             float mut = 0.f;
@@ -355,15 +370,15 @@ __global__ void __launch_bounds__(128) trace_kernel(const int4* __restrict__ rec
             const double zi = c0 ? z0 : (c1 ? z1 : z2);
             const double zn = c0 ? z1 : (c1 ? z2 : z0);
             const int idrop = c0 ? id2 : (c1 ? id0 : id1);  // slot i+2 leaves the face
-            const double wA = fmax(-si, 0.0), wQ = fmax(pn, 0.0), wR = fmax(-pi, 0.0);
+            // all three have exact sign -1/+1/-1; |.| differs from the clamp only when
+            // |value| <= tau (then by <= 2 tau, far below the chord tolerance)
+            const double wA = fabs(si), wQ = fabs(pn), wR = fabs(pi);
             const double sw = wA + wQ + wR;
             double zout;
             if (sw > 0.0) {
-                // offset from the apex; 1/sw from the fp32 reciprocal refined by
-                // one fp64 Newton step (rel. error ~2^-46)
-                double rin = (double)__frcp_rn((float)sw);
-                rin = rin * fma(-sw, rin, 2.0);
-                zout = fma(fma(wQ, zi - z3, wR * (zn - z3)), rin, z3);
+                // offset from the apex; 1/sw from the MUFU reciprocal refined by
+                // one fp64 Newton step (rel. error ~2^-40)
+                zout = fma(fma(wQ, zi - z3, wR * (zn - z3)), rcp_nr(sw), z3);
             } else {
                 zout = zin;
                 ++n_exact;
@@ -376,7 +391,7 @@ __global__ void __launch_bounds__(128) trace_kernel(const int4* __restrict__ rec
             }
             ++n_cross;
             // neighbour across the exit face = the face opposite the dropped vertex
-            const int lo = nodes.x == idrop ? 0 : nodes.y == idrop ? 1 : nodes.z == idrop ? 2 : 3;
+            const int lo = selp(0, selp(1, selp(2, 3, nodes.z == idrop), nodes.y == idrop), nodes.x == idrop);
             const int tag = sel4(tags, lo);
             if (tag < 0) break;
             if (++steps >= max_steps) { ++n_stuck; break; }
@@ -514,7 +529,7 @@ __global__ void __launch_bounds__(128, 4) walk_kernel(const int4* __restrict__ r
                     s01 = side2(x0, y0, x1, y1);
                     s12 = side2(x1, y1, x2, y2);
                     s20 = side2(x2, y2, x0, y0);
-                    const double w0 = fmax(-s12, 0.0), w1 = fmax(-s20, 0.0), w2 = fmax(-s01, 0.0);
+                    const double w0 = fabs(s12), w1 = fabs(s20), w2 = fabs(s01);
                     const double sw = w0 + w1 + w2;
                     zin = sw > 0 ? (w0 * z0 + w1 * z1 + w2 * z2) / sw : (z0 + z1 + z2) * (1.0 / 3.0);
                     sum = 0.0;
@@ -556,13 +571,13 @@ __global__ void __launch_bounds__(128, 4) walk_kernel(const int4* __restrict__ r
         const double zi = c0 ? z0 : (c1 ? z1 : z2);
         const double zn = c0 ? z1 : (c1 ? z2 : z0);
         const int idrop = c0 ? id2 : (c1 ? id0 : id1);
-        const double wA = fmax(-si, 0.0), wQ = fmax(pn, 0.0), wR = fmax(-pi, 0.0);
+        // all three have exact sign -1/+1/-1; |.| differs from the clamp only when
+            // |value| <= tau (then by <= 2 tau, far below the chord tolerance)
+            const double wA = fabs(si), wQ = fabs(pn), wR = fabs(pi);
         const double sw = wA + wQ + wR;
         double zout;
         if (sw > 0.0) {
-            double rin = (double)__frcp_rn((float)sw);
-            rin = rin * fma(-sw, rin, 2.0);
-            zout = fma(fma(wQ, zi - z3, wR * (zn - z3)), rin, z3);
+            zout = fma(fma(wQ, zi - z3, wR * (zn - z3)), rcp_nr(sw), z3);
         } else {
             zout = zin;
             ++n_exact;
@@ -574,7 +589,7 @@ __global__ void __launch_bounds__(128, 4) walk_kernel(const int4* __restrict__ r
             sum = fma(chord, (double)mut, sum);
         }
         ++n_cross;
-        const int lo = nodes.x == idrop ? 0 : nodes.y == idrop ? 1 : nodes.z == idrop ? 2 : 3;
+        const int lo = selp(0, selp(1, selp(2, 3, nodes.z == idrop), nodes.y == idrop), nodes.x == idrop);
         const int tag = sel4(tags, lo);
         ++steps;
         if (tag < 0 || steps >= max_steps) {
@@ -654,7 +669,7 @@ cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* en
                            const float* mu_int, float* proj, unsigned long long* stats,
                            cudaStream_t s) {
     trace_kernel<false><<<trace_grid(c), 128, 0, s>>>(m.rec, m.vtx, c.ang, c.beam, c.nv, c.nu,
-                                                      m.rmax, m.g, (long long)m.nt, entry,
+                                                      m.rmax, m.g, (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff), entry,
                                                       mu_int, proj, nullptr, nullptr, stats);
     return cudaGetLastError();
 }
@@ -663,7 +678,7 @@ cudaError_t launch_backward(const DevMesh& m, const LaunchChunk& c, const int* e
                             const float* y, double* acc, unsigned long long* stats,
                             cudaStream_t s) {
     trace_kernel<true><<<trace_grid(c), 128, 0, s>>>(m.rec, m.vtx, c.ang, c.beam, c.nv, c.nu,
-                                                     m.rmax, m.g, (long long)m.nt, entry,
+                                                     m.rmax, m.g, (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff), entry,
                                                      nullptr, nullptr, y, acc, stats);
     return cudaGetLastError();
 }
