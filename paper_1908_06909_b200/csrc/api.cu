@@ -111,12 +111,13 @@ void pool_setup(int dev) {
 
 enum class Op { Forward, Backward, BackwardF64 };
 
-// Walker selection (benchmarking knob): TETPROJ_WALK=tiled uses one thread per
-// pixel (trace_kernel); default is the persistent refill walker.
+// Walker selection (benchmarking knob): default is one thread per pixel in
+// 8x4-pixel warp tiles (trace_kernel, measured fastest: coherent tiles keep the
+// L1 hit rate high); TETPROJ_WALK=persistent selects the refill walker.
 int walker_mode() {
     static int mode = [] {
         const char* e = std::getenv("TETPROJ_WALK");
-        return (e && std::strcmp(e, "tiled") == 0) ? 1 : 0;
+        return (e && std::strcmp(e, "persistent") == 0) ? 0 : 1;
     }();
     return mode;
 }
