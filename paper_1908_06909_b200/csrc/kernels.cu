@@ -15,6 +15,7 @@
 // evaluation of the determinant and the 9-term SoS table.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "internal.h"
 
@@ -288,8 +289,8 @@ __global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ rec
         if (!out) { out = exact_side_ids(vtx, ang, beam, a, u, v, iap, id_other); ++n_exact; } \
     } while (0)
 
-template <bool BACK>
-__global__ void __launch_bounds__(128) trace_kernel(const int4* __restrict__ rec,
+template <bool BACK, int MINB>
+__global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict__ rec,
                                                     const int4* __restrict__ vtx,
                                                     const AngleGeom* __restrict__ ang, int beam,
                                                     int nv, int nu, double rmax, double g,
@@ -665,21 +666,49 @@ static dim3 trace_grid(const LaunchChunk& c) {
     return dim3(tiles, (unsigned)c.n_angles);
 }
 
+// Resident blocks per SM requested from ptxas (register cap 65536/(128*MINB));
+// TETPROJ_MINB overrides the default for measurements.
+static int trace_minb() {
+    static int v = [] {
+        const char* e = getenv("TETPROJ_MINB");
+        const int x = e ? atoi(e) : 4;
+        return (x == 5 || x == 6) ? x : 4;
+    }();
+    return v;
+}
+
+template <bool BACK>
+static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entry,
+                         const float* mu_int, float* proj, const float* y, double* acc,
+                         unsigned long long* stats, cudaStream_t s) {
+    const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
+    const dim3 grid = trace_grid(c);
+    switch (trace_minb()) {
+        case 5:
+            trace_kernel<BACK, 5><<<grid, 128, 0, s>>>(m.rec, m.vtx, c.ang, c.beam, c.nv, c.nu,
+                m.rmax, m.g, steps, entry, mu_int, proj, y, acc, stats);
+            break;
+        case 6:
+            trace_kernel<BACK, 6><<<grid, 128, 0, s>>>(m.rec, m.vtx, c.ang, c.beam, c.nv, c.nu,
+                m.rmax, m.g, steps, entry, mu_int, proj, y, acc, stats);
+            break;
+        default:
+            trace_kernel<BACK, 4><<<grid, 128, 0, s>>>(m.rec, m.vtx, c.ang, c.beam, c.nv, c.nu,
+                m.rmax, m.g, steps, entry, mu_int, proj, y, acc, stats);
+    }
+}
+
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
                            const float* mu_int, float* proj, unsigned long long* stats,
                            cudaStream_t s) {
-    trace_kernel<false><<<trace_grid(c), 128, 0, s>>>(m.rec, m.vtx, c.ang, c.beam, c.nv, c.nu,
-                                                      m.rmax, m.g, (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff), entry,
-                                                      mu_int, proj, nullptr, nullptr, stats);
+    launch_trace<false>(m, c, entry, mu_int, proj, nullptr, nullptr, stats, s);
     return cudaGetLastError();
 }
 
 cudaError_t launch_backward(const DevMesh& m, const LaunchChunk& c, const int* entry,
                             const float* y, double* acc, unsigned long long* stats,
                             cudaStream_t s) {
-    trace_kernel<true><<<trace_grid(c), 128, 0, s>>>(m.rec, m.vtx, c.ang, c.beam, c.nv, c.nu,
-                                                     m.rmax, m.g, (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff), entry,
-                                                     nullptr, nullptr, y, acc, stats);
+    launch_trace<true>(m, c, entry, nullptr, nullptr, y, acc, stats, s);
     return cudaGetLastError();
 }
 
