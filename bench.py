@@ -51,19 +51,21 @@ def dist_env():
 
 
 def rank_workload(cfg, rank, ws, angles_per_rank=None):
-    """The rank's share of an N-times-denser equidistant scan (weak scaling)."""
+    """Weak scaling: the full scan has ws*A equidistant angles and rank r owns
+    angles r::ws (paper_1908_06909_b200.dist.AngleSharding).  Returns the
+    workload, the FULL geometry, the rank's geometry and its detector rows."""
+    from paper_1908_06909_b200.dist import AngleSharding
     from workloads import configs as CF
-    from workloads import geometry as G
     w = CF.workload(cfg)
     A = angles_per_rank or w.geom.n_angles
     if cfg in ("c2", "c3", "c4b", "c5"):
-        # rebuild the circular scan with ws*A angles, take angles rank::ws
-        full = CF.workload(cfg, n_angles=A * ws)
-        geom = full.geom.subset(np.arange(rank, A * ws, ws))
+        full = CF.workload(cfg, n_angles=A * ws).geom
     else:
-        geom = w.geom.subset(np.arange(min(A, w.geom.n_angles)))
+        full = w.geom.subset(np.arange(min(A, w.geom.n_angles)))
+    sh = AngleSharding(full.n_angles, rank, ws)
+    geom = full.subset(sh.local_angles())
     y = CF.uniform_y(geom, 1000 + rank)
-    return w, geom, y
+    return w, full, geom, y
 
 
 class ClockSampler:
@@ -158,7 +160,7 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    w, geom, y = rank_workload(args.config, 0, 1, args.angles)
+    w, _, geom, y = rank_workload(args.config, 0, 1, args.angles)
     from oracle import tetref as O
     om = O.OracleMesh.from_mesh(w.mesh)
     cores = len(os.sched_getaffinity(0))
@@ -198,6 +200,7 @@ def main():
     import torch.distributed as dist
 
     from paper_1908_06909_b200 import tetproj as T
+    from paper_1908_06909_b200.dist import dist_backproject
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -206,7 +209,7 @@ def main():
     dev = torch.device("cuda", local)
     if ws > 1 and rank != 0:
         dist.barrier()                      # rank 0 builds the mesh cache first
-    w, geom, y_np = rank_workload(args.config, rank, ws, args.angles)
+    w, full_geom, geom, y_np = rank_workload(args.config, rank, ws, args.angles)
     if ws > 1 and rank == 0:
         dist.barrier()
     tm = T.TetMesh.from_mesh(w.mesh, device=local)
@@ -224,11 +227,16 @@ def main():
     assert st_f["lost"] == st_f["stuck"] == st_f["entry_conflicts"] == 0, st_f
     assert st_b["lost"] == st_b["stuck"] == 0, st_b
 
+    def backward():
+        if ws > 1:   # local A_r^T y_r, then all_reduce(SUM) over NCCL
+            dist_backproject(tm, full_geom, y,
+                             backproject=lambda g, yl: (T.tet_backproject(h, g, yl, x), x)[1])
+        else:
+            T.tet_backproject(h, geom, y, x)
+
     def step():
         T.tet_project(h, geom, mu, proj)
-        T.tet_backproject(h, geom, y, x)
-        if ws > 1:
-            dist.all_reduce(x)
+        backward()
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -247,9 +255,7 @@ def main():
             ev[i][0].record(stream)
             T.tet_project(h, geom, mu, proj)
             ev[i][1].record(stream)
-            T.tet_backproject(h, geom, y, x)
-            if ws > 1:
-                dist.all_reduce(x)
+            backward()
             ev[i][2].record(stream)
         torch.cuda.synchronize()
         if ws > 1:

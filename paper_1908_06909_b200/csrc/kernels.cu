@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
             const double sw = w0 + w1 + w2;
             zin = sw > 0 ? (w0 * z0 + w1 * z1 + w2 * z2) / sw : (z0 + z1 + z2) * (1.0 / 3.0);
         }
-        int steps = 0;
+        int steps_left = max_steps;
         while (true) {
             const int4 tags = ldg_nc_v4(rec + 2 * (size_t)t + 1);
             float mut = 0.f;
@@ -384,7 +384,9 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
                 zout = zin;
                 ++n_exact;
             }
-            const double chord = fmax((zout - zin) * F.scale, 0.0);
+            // (zout - zin) * scale >= 0 up to rounding; an exact zero-length
+            // crossing may come out as -1e-16 R, which is harmless in the sum
+            const double chord = (zout - zin) * F.scale;
             if (BACK) {
                 if (chord > 0.0) atomicAdd(acc + t, chord * (double)yv);
             } else {
@@ -392,10 +394,10 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
             }
             ++n_cross;
             // neighbour across the exit face = the face opposite the dropped vertex
-            const int lo = selp(0, selp(1, selp(2, 3, nodes.z == idrop), nodes.y == idrop), nodes.x == idrop);
-            const int tag = sel4(tags, lo);
+            const int tag = selp(tags.x, selp(tags.y, selp(tags.z, tags.w, nodes.z == idrop),
+                                              nodes.y == idrop), nodes.x == idrop);
             if (tag < 0) break;
-            if (++steps >= max_steps) { ++n_stuck; break; }
+            if (--steps_left == 0) { ++n_stuck; break; }
             t = tag >> 2;
             kin = tag & 3;
             nodes = ldg_nc_v4(rec + 2 * (size_t)t);

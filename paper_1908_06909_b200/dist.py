@@ -1,0 +1,79 @@
+"""Multi-GPU driver: projection angles sharded over ranks, mesh replicated,
+one all-reduce for the backprojection.
+
+"For our multi GPU approach, projections are divided, while keeping the full
+mesh in each of the GPUs memories".  The forward projection
+needs no communication (each rank owns the rows of its angles); the
+backprojection x = A^T y = sum_r A_r^T y_r is the only exchange: one
+``all_reduce(SUM)`` over the per-tet vector (NCCL over NVLink/NVSwitch on a
+B200 box; gloo in the CPU tests).
+
+The per-rank operators default to the CUDA library (TetMesh.project /
+TetMesh.backproject); they are parameters only so the host logic (sharding,
+geometry subsetting, reduction) can be exercised on CPU with another
+implementation of the same operator.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from types import SimpleNamespace
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class AngleSharding:
+    """Rank r of W owns angles r, r+W, r+2W, ... (interleaved, so angle-
+    dependent cost -- e.g. the silhouette of a box -- is balanced)."""
+    n_angles: int
+    rank: int
+    world: int
+
+    def __post_init__(self):
+        if not (0 <= self.rank < self.world) or self.n_angles < 1:
+            raise ValueError("bad sharding")
+
+    def local_angles(self) -> np.ndarray:
+        return np.arange(self.rank, self.n_angles, self.world)
+
+    def local_geometry(self, geom):
+        """Geometry restricted to this rank's angles (same beam / detector)."""
+        idx = self.local_angles()
+        return SimpleNamespace(beam=geom.beam, n_v=geom.n_v, n_u=geom.n_u,
+                               vecs=np.ascontiguousarray(np.asarray(geom.vecs)[idx]),
+                               n_angles=len(idx), n_rays=len(idx) * geom.n_v * geom.n_u)
+
+    def local_stack(self, y_full):
+        """This rank's rows of a full [A][Nv][Nu] detector stack."""
+        return y_full[self.local_angles()]
+
+
+def _world(group):
+    import torch.distributed as dist
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def sharding_for(geom, group=None) -> AngleSharding:
+    rank, world = _world(group)
+    return AngleSharding(geom.n_angles, rank, world)
+
+
+def dist_project(mesh, geom, mu, group=None, project=None):
+    """Forward projection of this rank's angles (no communication).
+    Returns (local_proj, sharding)."""
+    sh = sharding_for(geom, group)
+    fn = project if project is not None else mesh.project
+    return fn(sh.local_geometry(geom), mu), sh
+
+
+def dist_backproject(mesh, geom, y_local, group=None, backproject=None, async_op=False):
+    """x = A^T y over all ranks: local backprojection of this rank's angles,
+    then all_reduce(SUM).  ``y_local`` holds this rank's rows
+    (``AngleSharding.local_stack``).  Returns the reduced per-tet tensor
+    (or (tensor, work) when ``async_op``)."""
+    import torch.distributed as dist
+    sh = sharding_for(geom, group)
+    fn = backproject if backproject is not None else mesh.backproject
+    x = fn(sh.local_geometry(geom), y_local)
+    work = dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+    return (x, work) if async_op else x
