@@ -124,18 +124,19 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel):
-    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+def ncu_traffic(kernel, crossings_per_launch):
+    """DRAM bytes per launch of the walk kernel: ncu's dram__bytes_read.sum +
+    dram__bytes_write.sum per crossing (profiles/ncu_traffic.json, from one
+    `ncu --set full` capture of this bench's c3 launches) x crossings/launch."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        try:
-            return json.load(open(p)).get(kernel)
-        except Exception:
-            return None
-    return None
+    try:
+        per = json.load(open(p))[kernel]["dram_bytes_per_crossing"]
+        return per * crossings_per_launch
+    except Exception:
+        return None
 
 
-def cpu_baseline(w, geom, y, budget_angles=4):
+def cpu_baseline(w, geom, y, budget_angles=12):
     """The oracle as it stands, on this host's cores, on a bounded sample:
     `budget_angles` evenly spaced angles of the rank-0 scan, all pixels."""
     from oracle import tetref as O
@@ -353,7 +354,8 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
                          "bytes_per_crossing": bytes_unit,
-                         "traffic": ncu_traffic(dom),
+                         "traffic": ncu_traffic(dom, cross_unit / max(launches // args.steps, 1))
+                         if args.config == "c3" else None,
                          "per_launch_ms": per_launch_b if dom == "backward" else per_launch_f,
                          "note": "gathered bytes per crossing x crossings / walk-kernel time"},
             "e2e": {"value": e2e_value, "unit": "tet-crossings/s",
