@@ -19,6 +19,7 @@ struct tet_mesh {
     HostMesh host;      // keeps grid parameters (arrays freed after upload)
     DevMesh dev;
     void* d_rec = nullptr;
+    void* d_tnode = nullptr;
     void* d_vtx = nullptr;
     void* d_hull = nullptr;
     void* d_perm = nullptr;
@@ -110,26 +111,6 @@ void pool_setup(int dev) {
 }
 
 enum class Op { Forward, Backward, BackwardF64 };
-
-// Walker selection (benchmarking knob): default is one thread per pixel in
-// 8x4-pixel warp tiles (trace_kernel, measured fastest: coherent tiles keep the
-// L1 hit rate high); TETPROJ_WALK=persistent selects the refill walker.
-int walker_mode() {
-    static int mode = [] {
-        const char* e = std::getenv("TETPROJ_WALK");
-        return (e && std::strcmp(e, "persistent") == 0) ? 0 : 1;
-    }();
-    return mode;
-}
-
-int refill_threshold() {
-    static int r = [] {
-        const char* e = std::getenv("TETPROJ_REFILL");
-        int v = e ? std::atoi(e) : 16;
-        return v < 1 ? 1 : (v > 32 ? 32 : v);
-    }();
-    return r;
-}
 
 cudaEvent_t take_event(tet_mesh* m) {
     cudaEvent_t e = nullptr;
@@ -230,13 +211,6 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(g->n_angles, (1LL << 26) / per_angle));
         int* entry;
         CU(sc.alloc((void**)&entry, sizeof(int) * per_angle * chunk));
-        const bool persistent = walker_mode() == 0;
-        int2* list = nullptr;
-        unsigned* counters = nullptr;  // [0] hit-list length, [1] walker fetch cursor
-        if (persistent) {
-            CU(sc.alloc((void**)&list, sizeof(int2) * per_angle * chunk));
-            CU(sc.alloc((void**)&counters, 2 * sizeof(unsigned)));
-        }
         for (int a0 = 0; a0 < g->n_angles; a0 += chunk) {
             const int na = std::min(chunk, g->n_angles - a0);
             LaunchChunk c{d_ang + a0, d_aux + a0, g->beam, na, g->n_v, g->n_u};
@@ -247,17 +221,7 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
             }
             const size_t off = (size_t)a0 * per_angle;
             const bool fwd = op == Op::Forward;
-            if (persistent) {
-                CU(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned), s));
-                {
-                    KernelTimer kt(m, TET_K_ENTRY, s);
-                    CU(launch_hitlist(c, entry, list, counters, fwd ? (float*)d_out + off : nullptr, s));
-                }
-                KernelTimer kt(m, fwd ? TET_K_FORWARD : TET_K_BACKWARD, s);
-                CU(launch_walk(m->dev, c, !fwd, list, counters, counters + 1, refill_threshold(),
-                               mu_int, fwd ? (float*)d_out + off : nullptr, fwd ? nullptr : d_in + off,
-                               acc, d_stats, s));
-            } else if (fwd) {
+            if (fwd) {
                 KernelTimer kt(m, TET_K_FORWARD, s);
                 CU(launch_forward(m->dev, c, entry, mu_int, (float*)d_out + off, d_stats, s));
             } else {
@@ -330,6 +294,7 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
         return e;
     };
     cudaError_t e = up(&m->d_rec, H.rec.data(), H.rec.size() * 4);
+    if (e == cudaSuccess) e = up(&m->d_tnode, H.tnode.data(), H.tnode.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_vtx, H.vtx.data(), H.vtx.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_hull, H.hull.data(), H.hull.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_perm, H.perm.data(), H.perm.size() * 4);
@@ -338,6 +303,7 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
         return cuda_fail(e, "tet_mesh_create upload");
     }
     m->dev.rec = (const int4*)m->d_rec;
+    m->dev.tnode = (const int4*)m->d_tnode;
     m->dev.vtx = (const int4*)m->d_vtx;
     m->dev.hull = (const int2*)m->d_hull;
     m->dev.perm = (const int*)m->d_perm;
@@ -348,6 +314,7 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     m->dev.rmax = H.rmax;
     // host copies are no longer needed
     std::vector<int32_t>().swap(H.rec);
+    std::vector<int32_t>().swap(H.tnode);
     std::vector<int32_t>().swap(H.vtx);
     std::vector<int32_t>().swap(H.hull);
     std::vector<int32_t>().swap(H.perm);
@@ -364,6 +331,7 @@ tet_status tet_mesh_destroy(tet_mesh_t m) {
     }
     for (auto e : m->spare) cudaEventDestroy(e);
     cudaFree(m->d_rec);
+    cudaFree(m->d_tnode);
     cudaFree(m->d_vtx);
     cudaFree(m->d_hull);
     cudaFree(m->d_perm);

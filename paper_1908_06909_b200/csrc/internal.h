@@ -35,7 +35,8 @@ struct HostMesh {
     int e = 0;                 // grid exponent, g = 2^e
     double g = 0, C[3] = {0, 0, 0};
     std::vector<int32_t> vtx;  // [V][4] grid coords (x,y,z,0), internal vertex order
-    std::vector<int32_t> rec;  // [T][8] nodes(4) | nbr tags(4): (n<<2 | k') or -1
+    std::vector<int32_t> rec;  // [T][8] four face tags (lo, hi) -- see mesh_host.cpp
+    std::vector<int32_t> tnode;// [T][4] vertex ids (ray initialisation, entry finder)
     std::vector<int32_t> hull; // [B][2] (t, k) internal order
     std::vector<int32_t> perm; // [T] internal -> caller tet index
     double rmax = 0;           // max |X|_2 over vertices (grid units)
@@ -56,7 +57,8 @@ tet_status prepare_geometry(const HostMesh& m, const tet_geometry* g,
 
 // ------------------------------------------------------------- device ----
 struct DevMesh {
-    const int4* rec = nullptr;   // [2T]
+    const int4* rec = nullptr;   // [2T] face tags
+    const int4* tnode = nullptr; // [T] node ids
     const int4* vtx = nullptr;   // [V]
     const int2* hull = nullptr;  // [B]
     const int* perm = nullptr;   // [T]
@@ -84,12 +86,6 @@ cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* en
 cudaError_t launch_backward(const DevMesh& m, const LaunchChunk& c, const int* entry,
                             const float* y, double* acc, unsigned long long* stats,
                             cudaStream_t s);
-cudaError_t launch_hitlist(const LaunchChunk& c, const int* entry, int2* list, unsigned* count,
-                           float* proj, cudaStream_t s);
-cudaError_t launch_walk(const DevMesh& m, const LaunchChunk& c, bool back, const int2* list,
-                        const unsigned* count, unsigned* next, int refill, const float* mu_int,
-                        float* proj, const float* y, double* acc, unsigned long long* stats,
-                        cudaStream_t s);
 cudaError_t launch_gather_mu(const DevMesh& m, const float* mu, float* mu_int,
                              cudaStream_t s);
 cudaError_t launch_scatter_x(const DevMesh& m, const double* acc, float* x, int accumulate,

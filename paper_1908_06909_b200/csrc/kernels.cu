@@ -3,7 +3,7 @@
 //   entry_kernel      hull-entry finder: per (hull face,
 //                     angle) block, exact test of every pixel in the face's
 //                     detector footprint; writes entry[ray] = tet<<2 | k.
-//   trace_kernel<B>   ray walk (a4) + forward accumulate (a5, B=false) or
+//   trace_kernel<B,M> ray walk (a4) + forward accumulate (a5, B=false) or
 //                     backprojection scatter (a6, B=true).  Alg. 2 of the
 //                     paper with exact sign decisions.
 //   gather / scatter  caller order <-> internal SFC order (K4).
@@ -192,7 +192,7 @@ __device__ __forceinline__ int side_direct(const int4 a, const int4 b, const Ray
     return sos_side(a.x, a.y, a.z, b.x, b.y, b.z, r.ox, r.oy, r.oz, r.px, r.py, r.pz);
 }
 
-__global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ rec,
+__global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ tnode,
                                                     const int4* __restrict__ vtx,
                                                     const int2* __restrict__ hull,
                                                     const AngleGeom* __restrict__ ang,
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ rec
                                                     unsigned long long* __restrict__ stats) {
     const int h = blockIdx.x, a = blockIdx.y;
     const int2 hk = hull[h];
-    const int4 nodes = ldg_nc_v4(rec + 2 * (size_t)hk.x);
+    const int4 nodes = __ldg(tnode + hk.x);
     const int k = hk.y;
     // outward order of face k (opposite node k)
     int ia, ib, ic;
@@ -289,19 +289,27 @@ __global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ rec
         if (!out) { out = exact_side_ids(vtx, ang, beam, a, u, v, iap, id_other); ++n_exact; } \
     } while (0)
 
+// One thread per ray, 8x4-pixel warp tiles (16x8 per block).
+// State: the entry face in three fixed slots k = 0,1,2 in cyclic order (shear
+// coordinates x', y', z', vertex id, local index l_k in the current tet) with
+// the edge sides s01, s12, s20 (exact sign -1), the apex id `iap` (from the
+// previous face tag), the entry depth zin.  Per step the face tags of t and
+// the apex vertex are gathered IN PARALLEL (the tag carried the apex id);
+// the tag of the exit face gives the next tet, its apex and the local-index
+// map, so the neighbour's node list is never loaded.
 template <bool BACK, int MINB>
 __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict__ rec,
-                                                    const int4* __restrict__ vtx,
-                                                    const AngleGeom* __restrict__ ang, int beam,
-                                                    int nv, int nu, double rmax, double g,
-                                                    int max_steps,
-                                                    const int* __restrict__ entry,
-                                                    const float* __restrict__ mu,
-                                                    float* __restrict__ proj,
-                                                    const float* __restrict__ y,
-                                                    double* __restrict__ acc,
-                                                    unsigned long long* __restrict__ stats) {
-    // 16x8 pixel tile per block, 8x4 per warp
+                                                          const int4* __restrict__ tnode,
+                                                          const int4* __restrict__ vtx,
+                                                          const AngleGeom* __restrict__ ang,
+                                                          int beam, int nv, int nu, double rmax,
+                                                          double g, int max_steps,
+                                                          const int* __restrict__ entry,
+                                                          const float* __restrict__ mu,
+                                                          float* __restrict__ proj,
+                                                          const float* __restrict__ y,
+                                                          double* __restrict__ acc,
+                                                          unsigned long long* __restrict__ stats) {
     const int tiles_u = (nu + 15) >> 4;
     const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
     const int a = blockIdx.y;
@@ -320,14 +328,14 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
         make_frame(r, rmax, g, F);
         const float yv = BACK ? y[rid] : 0.f;
         int t = e >> 2, kin = e & 3;
-        int4 nodes = ldg_nc_v4(rec + 2 * (size_t)t);
-        // three vertex slots holding the entry face in cyclic order; their edge
-        // sides s01, s12, s20 all have exact sign -1 (entering, R3)
-        int id0, id1, id2;
-        if (kin == 0)      { id0 = nodes.y; id1 = nodes.z; id2 = nodes.w; }
-        else if (kin == 1) { id0 = nodes.x; id1 = nodes.w; id2 = nodes.z; }
-        else if (kin == 2) { id0 = nodes.x; id1 = nodes.y; id2 = nodes.w; }
-        else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; }
+        const int4 nodes = __ldg(tnode + t);
+        // entry face = face kin in outward order (opposite node kin)
+        int id0, id1, id2, lp;
+        if (kin == 0)      { id0 = nodes.y; id1 = nodes.z; id2 = nodes.w; lp = 1 | 2 << 2 | 3 << 4; }
+        else if (kin == 1) { id0 = nodes.x; id1 = nodes.w; id2 = nodes.z; lp = 0 | 3 << 2 | 2 << 4; }
+        else if (kin == 2) { id0 = nodes.x; id1 = nodes.y; id2 = nodes.w; lp = 0 | 1 << 2 | 3 << 4; }
+        else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; lp = 0 | 2 << 2 | 1 << 4; }
+        int iap = sel4(nodes, kin);
         double x0, y0, z0, x1, y1, z1, x2, y2, z2;
         xform(F, __ldg(vtx + id0), x0, y0, z0);
         xform(F, __ldg(vtx + id1), x1, y1, z1);
@@ -341,10 +349,11 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
         }
         int steps_left = max_steps;
         while (true) {
-            const int4 tags = ldg_nc_v4(rec + 2 * (size_t)t + 1);
+            // independent gathers: face tags of t (32 B), apex vertex (16 B), mu (4 B)
+            const int4 ta = ldg_nc_v4(rec + 2 * (size_t)t);
+            const int4 tb = ldg_nc_v4(rec + 2 * (size_t)t + 1);
             float mut = 0.f;
             if (!BACK) mut = __ldg(mu + t);
-            const int iap = sel4(nodes, kin);  // apex: node opposite the entry face
             double x3, y3, z3;
             xform(F, __ldg(vtx + iap), x3, y3, z3);
             const double p0 = side2(x3, y3, x0, y0);   // side(apex, slot k)
@@ -364,13 +373,12 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
                 if (i == 1 && p1 > F.tau) ++n_lost;    // (+,+,+) is impossible
             }
             const bool c0 = i == 0, c1 = i == 1;
-            // crossing point weights: apex -s(i,i+1), slot i p_{i+1}, slot i+1 -p_i
+            // crossing point weights: apex |s(i,i+1)|, slot i |p_{i+1}|, slot i+1 |p_i|
             const double si = c0 ? s01 : (c1 ? s12 : s20);
             const double pi = c0 ? p0 : (c1 ? p1 : p2);
             const double pn = c0 ? p1 : (c1 ? p2 : p0);
             const double zi = c0 ? z0 : (c1 ? z1 : z2);
             const double zn = c0 ? z1 : (c1 ? z2 : z0);
-            const int idrop = c0 ? id2 : (c1 ? id0 : id1);  // slot i+2 leaves the face
             // all three have exact sign -1/+1/-1; |.| differs from the clamp only when
             // |value| <= tau (then by <= 2 tau, far below the chord tolerance)
             const double wA = fabs(si), wQ = fabs(pn), wR = fabs(pi);
@@ -393,25 +401,33 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
                 sum = fma(chord, (double)mut, sum);
             }
             ++n_cross;
-            // neighbour across the exit face = the face opposite the dropped vertex
-            const int tag = selp(tags.x, selp(tags.y, selp(tags.z, tags.w, nodes.z == idrop),
-                                              nodes.y == idrop), nodes.x == idrop);
-            if (tag < 0) break;
+            // exit through the face opposite slot i+2 (local index L in t)
+            const int j = selp(2, selp(0, 1, c1), c0);
+            const int L = (lp >> (2 * j)) & 3;
+            const int lo = selp(selp(ta.x, ta.z, L == 0), selp(tb.x, tb.z, L == 2), L < 2);
+            if (lo < 0) break;
             if (--steps_left == 0) { ++n_stuck; break; }
-            t = tag >> 2;
-            kin = tag & 3;
-            nodes = ldg_nc_v4(rec + 2 * (size_t)t);
+            const unsigned hi = (unsigned)selp(selp(ta.y, ta.w, L == 0), selp(tb.y, tb.w, L == 2), L < 2);
+            // local indices in the next tet: kept slots map through `map`, the
+            // dropped slot j receives the current apex (local index kin)
+            const bool d0 = j == 0, d1 = j == 1, d2 = j == 2;
+            const int s0 = selp(kin, lp & 3, d0);
+            const int s1 = selp(kin, (lp >> 2) & 3, d1);
+            const int s2 = selp(kin, (lp >> 4) & 3, d2);
+            lp = ((hi >> (2 * s0)) & 3) | (((hi >> (2 * s1)) & 3) << 2) | (((hi >> (2 * s2)) & 3) << 4);
+            t = lo >> 2;
+            kin = lo & 3;
             // the apex takes the dropped slot i+2; cyclic order is preserved
-            const bool d0 = i == 1, d1 = i == 2, d2 = i == 0;
-            x0 = d0 ? x3 : x0; y0 = d0 ? y3 : y0; z0 = d0 ? z3 : z0; id0 = d0 ? iap : id0;
-            x1 = d1 ? x3 : x1; y1 = d1 ? y3 : y1; z1 = d1 ? z3 : z1; id1 = d1 ? iap : id1;
-            x2 = d2 ? x3 : x2; y2 = d2 ? y3 : y2; z2 = d2 ? z3 : z2; id2 = d2 ? iap : id2;
+            x0 = d0 ? x3 : x0; y0 = d0 ? y3 : y0; z0 = d0 ? z3 : z0; id0 = selp(iap, id0, d0);
+            x1 = d1 ? x3 : x1; y1 = d1 ? y3 : y1; z1 = d1 ? z3 : z1; id1 = selp(iap, id1, d1);
+            x2 = d2 ? x3 : x2; y2 = d2 ? y3 : y2; z2 = d2 ? z3 : z2; id2 = selp(iap, id2, d2);
             // s_{i+1} <- -p_{i+1}, s_{i+2} <- p_i
             const double n01 = c1 ? p1 : (d1 ? -p0 : s01);
             const double n12 = c0 ? -p1 : (d1 ? p2 : s12);
             const double n20 = c0 ? p0 : (c1 ? -p2 : s20);
             s01 = n01; s12 = n12; s20 = n20;
             zin = zout;
+            iap = (int)(hi >> 8);
         }
     }
     if (!BACK && valid) proj[rid] = (float)sum;
@@ -421,207 +437,6 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
     add_stat(stats, ST_LOST, n_lost);
     add_stat(stats, ST_STUCK, n_stuck);
     const unsigned mx = __reduce_max_sync(0xffffffffu, n_cross);
-    if (lane == 0 && mx) atomicMax(stats + ST_MAXC, (unsigned long long)mx);
-}
-
-// ----------------------------------------------------------- hit list ---
-// Compacts the rays that enter the mesh, one 8x4-pixel warp tile at a time,
-// so the persistent walker below reads coherent groups of rays; in forward
-// mode it also writes 0 for the rays that miss the mesh (Alg. 2 "Return if
-// i_now = -1").
-__global__ void __launch_bounds__(128) hitlist_kernel(const int* __restrict__ entry, int nv,
-                                                      int nu, int2* __restrict__ list,
-                                                      unsigned* __restrict__ count,
-                                                      float* __restrict__ proj) {
-    const int tiles_u = (nu + 15) >> 4;
-    const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
-    const int a = blockIdx.y;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int u = bx * 16 + (w & 1) * 8 + (lane & 7);
-    const int v = by * 8 + (w >> 1) * 4 + (lane >> 3);
-    const bool valid = u < nu && v < nv;
-    const int rid = (a * nv + v) * nu + u;
-    const int e = valid ? entry[rid] : -1;
-    if (proj && valid && e < 0) proj[rid] = 0.f;
-    const unsigned m = __ballot_sync(0xffffffffu, e >= 0);
-    if (!m) return;
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(count, (unsigned)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (e >= 0) list[base + __popc(m & ((1u << lane) - 1u))] = make_int2(rid, e);
-}
-
-// Exact sign for vertex ids ia, ib of chunk-local ray `rid` (rare path).
-__device__ __noinline__ int exact_side_rid(const int4* __restrict__ vtx,
-                                           const AngleGeom* __restrict__ ang, int beam, int nv,
-                                           int nu, int rid, int ia, int ib) {
-    const int per = nv * nu;
-    const int a = rid / per, rem = rid - a * per;
-    const int v = rem / nu, u = rem - v * nu;
-    return exact_side_ids(vtx, ang, beam, a, u, v, ia, ib);
-}
-
-#define SIGN_R(val, id_other, out)                                                     \
-    do {                                                                             \
-        out = (val) > F.tau ? 1 : ((val) < -F.tau ? -1 : 0);                         \
-        if (!out) {                                                                  \
-            out = exact_side_rid(vtx, ang, beam, nv, nu, rid, iap, id_other);        \
-            ++n_exact;                                                               \
-        }                                                                            \
-    } while (0)
-
-// Persistent walker (a4-a6): a grid of resident warps pulls rays from the
-// hit list; a lane whose ray has left the mesh idles until `refill` lanes of
-// its warp are idle, then the idle lanes fetch new rays together (ray
-// refill keeps lanes busy despite ray-length variance; PAPER.md:165 notes
-// the divergence problem of one-thread-per-pixel launches).
-template <bool BACK>
-__global__ void __launch_bounds__(128, 4) walk_kernel(const int4* __restrict__ rec,
-                                                      const int4* __restrict__ vtx,
-                                                      const AngleGeom* __restrict__ ang, int beam,
-                                                      int nv, int nu, double rmax, double g,
-                                                      int max_steps, const int2* __restrict__ list,
-                                                      const unsigned* __restrict__ count,
-                                                      unsigned* __restrict__ next, int refill,
-                                                      const float* __restrict__ mu,
-                                                      float* __restrict__ proj,
-                                                      const float* __restrict__ y,
-                                                      double* __restrict__ acc,
-                                                      unsigned long long* __restrict__ stats) {
-    const int lane = threadIdx.x & 31;
-    const unsigned lanemask_lt = (1u << lane) - 1u;
-    const unsigned n_hit = *count;
-    unsigned n_cross = 0, n_exact = 0, n_lost = 0, n_stuck = 0, max_cross = 0, n_done = 0;
-    bool active = false, drained = false;
-    // ray state
-    Frame F;
-    int rid = 0, t = 0, kin = 0, steps = 0, id0 = 0, id1 = 0, id2 = 0;
-    int4 nodes = make_int4(0, 0, 0, 0);
-    double x0 = 0, y0 = 0, z0 = 0, x1 = 0, y1 = 0, z1 = 0, x2 = 0, y2 = 0, z2 = 0;
-    double s01 = 0, s12 = 0, s20 = 0, zin = 0, sum = 0;
-    float yv = 0.f;
-    while (true) {
-        if (!drained) {
-            const unsigned idle = __ballot_sync(0xffffffffu, !active);
-            if (__popc(idle) >= refill || idle == 0xffffffffu) {
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(next, (unsigned)__popc(idle));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (base + __popc(idle) >= n_hit) drained = true;
-                const unsigned j = base + __popc(idle & lanemask_lt);
-                if (!active && j < n_hit) {
-                    // ---- ray init: frame, entry face slots, entry depth
-                    const int2 it = list[j];
-                    rid = it.x;
-                    const int per = nv * nu;
-                    const int a = rid / per, rem = rid - a * per;
-                    const int v = rem / nu, u = rem - v * nu;
-                    const RayPts r = ray_points(ang[a], beam, u, v);
-                    make_frame(r, rmax, g, F);
-                    if (BACK) yv = y[rid];
-                    t = it.y >> 2;
-                    kin = it.y & 3;
-                    nodes = ldg_nc_v4(rec + 2 * (size_t)t);
-                    if (kin == 0)      { id0 = nodes.y; id1 = nodes.z; id2 = nodes.w; }
-                    else if (kin == 1) { id0 = nodes.x; id1 = nodes.w; id2 = nodes.z; }
-                    else if (kin == 2) { id0 = nodes.x; id1 = nodes.y; id2 = nodes.w; }
-                    else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; }
-                    xform(F, __ldg(vtx + id0), x0, y0, z0);
-                    xform(F, __ldg(vtx + id1), x1, y1, z1);
-                    xform(F, __ldg(vtx + id2), x2, y2, z2);
-                    s01 = side2(x0, y0, x1, y1);
-                    s12 = side2(x1, y1, x2, y2);
-                    s20 = side2(x2, y2, x0, y0);
-                    const double w0 = fabs(s12), w1 = fabs(s20), w2 = fabs(s01);
-                    const double sw = w0 + w1 + w2;
-                    zin = sw > 0 ? (w0 * z0 + w1 * z1 + w2 * z2) / sw : (z0 + z1 + z2) * (1.0 / 3.0);
-                    sum = 0.0;
-                    steps = 0;
-                    active = true;
-                }
-            }
-        }
-        if (!__any_sync(0xffffffffu, active)) {
-            if (drained) break;
-            continue;
-        }
-        if (!active) continue;
-        // ---- one traversal step (same rule as trace_kernel)
-        const int4 tags = ldg_nc_v4(rec + 2 * (size_t)t + 1);
-        float mut = 0.f;
-        if (!BACK) mut = __ldg(mu + t);
-        const int iap = sel4(nodes, kin);
-        double x3, y3, z3;
-        xform(F, __ldg(vtx + iap), x3, y3, z3);
-        const double p0 = side2(x3, y3, x0, y0);
-        const double p1 = side2(x3, y3, x1, y1);
-        const double p2 = side2(x3, y3, x2, y2);
-        int sa, sb, i;
-        SIGN_R(p0, id0, sa);
-        if (sa < 0) {
-            SIGN_R(p1, id1, sb);
-            i = sb > 0 ? 0 : 1;
-            if (i == 1 && p2 < -F.tau) ++n_lost;
-        } else {
-            SIGN_R(p2, id2, sb);
-            i = sb < 0 ? 2 : 1;
-            if (i == 1 && p1 > F.tau) ++n_lost;
-        }
-        const bool c0 = i == 0, c1 = i == 1;
-        const double si = c0 ? s01 : (c1 ? s12 : s20);
-        const double pi = c0 ? p0 : (c1 ? p1 : p2);
-        const double pn = c0 ? p1 : (c1 ? p2 : p0);
-        const double zi = c0 ? z0 : (c1 ? z1 : z2);
-        const double zn = c0 ? z1 : (c1 ? z2 : z0);
-        const int idrop = c0 ? id2 : (c1 ? id0 : id1);
-        // all three have exact sign -1/+1/-1; |.| differs from the clamp only when
-            // |value| <= tau (then by <= 2 tau, far below the chord tolerance)
-            const double wA = fabs(si), wQ = fabs(pn), wR = fabs(pi);
-        const double sw = wA + wQ + wR;
-        double zout;
-        if (sw > 0.0) {
-            zout = fma(fma(wQ, zi - z3, wR * (zn - z3)), rcp_nr(sw), z3);
-        } else {
-            zout = zin;
-            ++n_exact;
-        }
-        const double chord = fmax((zout - zin) * F.scale, 0.0);
-        if (BACK) {
-            if (chord > 0.0) atomicAdd(acc + t, chord * (double)yv);
-        } else {
-            sum = fma(chord, (double)mut, sum);
-        }
-        ++n_cross;
-        const int lo = selp(0, selp(1, selp(2, 3, nodes.z == idrop), nodes.y == idrop), nodes.x == idrop);
-        const int tag = sel4(tags, lo);
-        ++steps;
-        if (tag < 0 || steps >= max_steps) {
-            if (tag >= 0) ++n_stuck;
-            if (!BACK) proj[rid] = (float)sum;
-            max_cross = max(max_cross, (unsigned)steps);
-            ++n_done;
-            active = false;
-            continue;
-        }
-        t = tag >> 2;
-        kin = tag & 3;
-        nodes = ldg_nc_v4(rec + 2 * (size_t)t);
-        const bool d0 = i == 1, d1 = i == 2, d2 = i == 0;
-        x0 = d0 ? x3 : x0; y0 = d0 ? y3 : y0; z0 = d0 ? z3 : z0; id0 = d0 ? iap : id0;
-        x1 = d1 ? x3 : x1; y1 = d1 ? y3 : y1; z1 = d1 ? z3 : z1; id1 = d1 ? iap : id1;
-        x2 = d2 ? x3 : x2; y2 = d2 ? y3 : y2; z2 = d2 ? z3 : z2; id2 = d2 ? iap : id2;
-        const double n01 = c1 ? p1 : (d1 ? -p0 : s01);
-        const double n12 = c0 ? -p1 : (d1 ? p2 : s12);
-        const double n20 = c0 ? p0 : (c1 ? -p2 : s20);
-        s01 = n01; s12 = n12; s20 = n20;
-        zin = zout;
-    }
-    add_stat(stats, ST_HIT, n_done);
-    add_stat(stats, ST_CROSS, n_cross);
-    add_stat(stats, ST_EXACT, n_exact);
-    add_stat(stats, ST_LOST, n_lost);
-    add_stat(stats, ST_STUCK, n_stuck);
-    const unsigned mx = __reduce_max_sync(0xffffffffu, max_cross);
     if (lane == 0 && mx) atomicMax(stats + ST_MAXC, (unsigned long long)mx);
 }
 
@@ -658,7 +473,7 @@ static int grid_for(int64_t n) {
 cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry,
                          unsigned long long* stats, cudaStream_t s) {
     dim3 grid((unsigned)m.nb, (unsigned)c.n_angles);
-    entry_kernel<<<grid, 256, 0, s>>>(m.rec, m.vtx, m.hull, c.ang, c.aux, c.beam, c.nv, c.nu,
+    entry_kernel<<<grid, 256, 0, s>>>(m.tnode, m.vtx, m.hull, c.ang, c.aux, c.beam, c.nv, c.nu,
                                       entry, stats);
     return cudaGetLastError();
 }
@@ -687,15 +502,15 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     const dim3 grid = trace_grid(c);
     switch (trace_minb()) {
         case 5:
-            trace_kernel<BACK, 5><<<grid, 128, 0, s>>>(m.rec, m.vtx, c.ang, c.beam, c.nv, c.nu,
+            trace_kernel<BACK, 5><<<grid, 128, 0, s>>>(m.rec, m.tnode, m.vtx, c.ang, c.beam, c.nv, c.nu,
                 m.rmax, m.g, steps, entry, mu_int, proj, y, acc, stats);
             break;
         case 6:
-            trace_kernel<BACK, 6><<<grid, 128, 0, s>>>(m.rec, m.vtx, c.ang, c.beam, c.nv, c.nu,
+            trace_kernel<BACK, 6><<<grid, 128, 0, s>>>(m.rec, m.tnode, m.vtx, c.ang, c.beam, c.nv, c.nu,
                 m.rmax, m.g, steps, entry, mu_int, proj, y, acc, stats);
             break;
         default:
-            trace_kernel<BACK, 4><<<grid, 128, 0, s>>>(m.rec, m.vtx, c.ang, c.beam, c.nv, c.nu,
+            trace_kernel<BACK, 4><<<grid, 128, 0, s>>>(m.rec, m.tnode, m.vtx, c.ang, c.beam, c.nv, c.nu,
                 m.rmax, m.g, steps, entry, mu_int, proj, y, acc, stats);
     }
 }
@@ -711,42 +526,6 @@ cudaError_t launch_backward(const DevMesh& m, const LaunchChunk& c, const int* e
                             const float* y, double* acc, unsigned long long* stats,
                             cudaStream_t s) {
     launch_trace<true>(m, c, entry, nullptr, nullptr, y, acc, stats, s);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_hitlist(const LaunchChunk& c, const int* entry, int2* list, unsigned* count,
-                           float* proj, cudaStream_t s) {
-    hitlist_kernel<<<trace_grid(c), 128, 0, s>>>(entry, c.nv, c.nu, list, count, proj);
-    return cudaGetLastError();
-}
-
-static int walk_blocks(const void* fn) {
-    static int cached[2] = {0, 0};
-    const int idx = fn == (const void*)walk_kernel<true> ? 1 : 0;
-    if (!cached[idx]) {
-        int dev = 0, sms = 148, per = 4;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 128, 0);
-        cached[idx] = sms * (per > 0 ? per : 1);
-    }
-    return cached[idx];
-}
-
-cudaError_t launch_walk(const DevMesh& m, const LaunchChunk& c, bool back, const int2* list,
-                        const unsigned* count, unsigned* next, int refill, const float* mu_int,
-                        float* proj, const float* y, double* acc, unsigned long long* stats,
-                        cudaStream_t s) {
-    const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
-    if (back) {
-        walk_kernel<true><<<walk_blocks((const void*)walk_kernel<true>), 128, 0, s>>>(
-            m.rec, m.vtx, c.ang, c.beam, c.nv, c.nu, m.rmax, m.g, steps, list, count, next, refill,
-            nullptr, nullptr, y, acc, stats);
-    } else {
-        walk_kernel<false><<<walk_blocks((const void*)walk_kernel<false>), 128, 0, s>>>(
-            m.rec, m.vtx, c.ang, c.beam, c.nv, c.nu, m.rmax, m.g, steps, list, count, next, refill,
-            mu_int, proj, nullptr, nullptr, stats);
-    }
     return cudaGetLastError();
 }
 
