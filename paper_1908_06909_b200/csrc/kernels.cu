@@ -373,12 +373,12 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
                 if (i == 1 && p1 > F.tau) ++n_lost;    // (+,+,+) is impossible
             }
             const bool c0 = i == 0, c1 = i == 1;
-            // crossing point weights: apex |s(i,i+1)|, slot i |p_{i+1}|, slot i+1 |p_i|
-            const double si = c0 ? s01 : (c1 ? s12 : s20);
-            const double pi = c0 ? p0 : (c1 ? p1 : p2);
-            const double pn = c0 ? p1 : (c1 ? p2 : p0);
-            const double zi = c0 ? z0 : (c1 ? z1 : z2);
-            const double zn = c0 ? z1 : (c1 ? z2 : z0);
+            // crossing point weights: apex |s(i,i+1)|, slot i |p_{i+1}|, slot i+1 |p_i|.
+            // Selections are written as predicated moves (IMAD.MOV on the FMA
+            // pipe) rather than FSELs: the ALU pipe is the walker's hot pipe.
+            double si = s20, pi = p2, pn = p0, zi = z2, zn = z0;
+            if (c0) { si = s01; pi = p0; pn = p1; zi = z0; zn = z1; }
+            if (c1) { si = s12; pi = p1; pn = p2; zi = z1; zn = z2; }
             // all three have exact sign -1/+1/-1; |.| differs from the clamp only when
             // |value| <= tau (then by <= 2 tau, far below the chord tolerance)
             const double wA = fabs(si), wQ = fabs(pn), wR = fabs(pi);
@@ -417,15 +417,11 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
             lp = ((hi >> (2 * s0)) & 3) | (((hi >> (2 * s1)) & 3) << 2) | (((hi >> (2 * s2)) & 3) << 4);
             t = lo >> 2;
             kin = lo & 3;
-            // the apex takes the dropped slot i+2; cyclic order is preserved
-            x0 = d0 ? x3 : x0; y0 = d0 ? y3 : y0; z0 = d0 ? z3 : z0; id0 = selp(iap, id0, d0);
-            x1 = d1 ? x3 : x1; y1 = d1 ? y3 : y1; z1 = d1 ? z3 : z1; id1 = selp(iap, id1, d1);
-            x2 = d2 ? x3 : x2; y2 = d2 ? y3 : y2; z2 = d2 ? z3 : z2; id2 = selp(iap, id2, d2);
+            // the apex takes the dropped slot i+2 (cyclic order is preserved);
             // s_{i+1} <- -p_{i+1}, s_{i+2} <- p_i
-            const double n01 = c1 ? p1 : (d1 ? -p0 : s01);
-            const double n12 = c0 ? -p1 : (d1 ? p2 : s12);
-            const double n20 = c0 ? p0 : (c1 ? -p2 : s20);
-            s01 = n01; s12 = n12; s20 = n20;
+            if (d0) { x0 = x3; y0 = y3; z0 = z3; id0 = iap; s20 = -p2; s01 = p1; }
+            if (d1) { x1 = x3; y1 = y3; z1 = z3; id1 = iap; s01 = -p0; s12 = p2; }
+            if (d2) { x2 = x3; y2 = y3; z2 = z3; id2 = iap; s12 = -p1; s20 = p0; }
             zin = zout;
             iap = (int)(hi >> 8);
         }
