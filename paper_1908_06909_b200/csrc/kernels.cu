@@ -348,14 +348,18 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
             zin = sw > 0 ? (w0 * z0 + w1 * z1 + w2 * z2) / sw : (z0 + z1 + z2) * (1.0 / 3.0);
         }
         int steps_left = max_steps;
+        // Software-pipelined by one step: the gathers of step k+1 (face tags of
+        // the next tet, its apex vertex, mu) are issued as soon as step k's
+        // exit face is known, and step k's chord / accumulation / slot update
+        // run while they are in flight.
+        int4 ta = ldg_nc_v4(rec + 2 * (size_t)t);          // face tags of t (32 B)
+        int4 tb = ldg_nc_v4(rec + 2 * (size_t)t + 1);
+        float mut = 0.f;
+        if (!BACK) mut = __ldg(mu + t);
+        int4 X = __ldg(vtx + iap);                          // apex vertex (16 B)
         while (true) {
-            // independent gathers: face tags of t (32 B), apex vertex (16 B), mu (4 B)
-            const int4 ta = ldg_nc_v4(rec + 2 * (size_t)t);
-            const int4 tb = ldg_nc_v4(rec + 2 * (size_t)t + 1);
-            float mut = 0.f;
-            if (!BACK) mut = __ldg(mu + t);
             double x3, y3, z3;
-            xform(F, __ldg(vtx + iap), x3, y3, z3);
+            xform(F, X, x3, y3, z3);
             const double p0 = side2(x3, y3, x0, y0);   // side(apex, slot k)
             const double p1 = side2(x3, y3, x1, y1);
             const double p2 = side2(x3, y3, x2, y2);
@@ -373,6 +377,31 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
                 if (i == 1 && p1 > F.tau) ++n_lost;    // (+,+,+) is impossible
             }
             const bool c0 = i == 0, c1 = i == 1;
+            // exit through the face opposite slot j = i+2 (local index L in t)
+            const int j = selp(2, selp(0, 1, c1), c0);
+            const int L = (lp >> (2 * j)) & 3;
+            const int lo = selp(selp(ta.x, ta.z, L == 0), selp(tb.x, tb.z, L == 2), L < 2);
+            const unsigned hi = (unsigned)selp(selp(ta.y, ta.w, L == 0), selp(tb.y, tb.w, L == 2), L < 2);
+            const bool more = lo >= 0 && --steps_left != 0;
+            const int tcur = t;
+            const float mcur = mut;
+            const bool d0 = j == 0, d1 = j == 1, d2 = j == 2;
+            if (more) {
+                t = lo >> 2;
+                ta = ldg_nc_v4(rec + 2 * (size_t)t);
+                tb = ldg_nc_v4(rec + 2 * (size_t)t + 1);
+                if (!BACK) mut = __ldg(mu + t);
+                X = __ldg(vtx + (int)(hi >> 8));
+                // local indices in the next tet: kept slots map through `map`,
+                // the dropped slot j receives the current apex (local index kin)
+                const int s0 = selp(kin, lp & 3, d0);
+                const int s1 = selp(kin, (lp >> 2) & 3, d1);
+                const int s2 = selp(kin, (lp >> 4) & 3, d2);
+                lp = ((hi >> (2 * s0)) & 3) | (((hi >> (2 * s1)) & 3) << 2) |
+                     (((hi >> (2 * s2)) & 3) << 4);
+                kin = lo & 3;
+            }
+            // ---- chord of step k (overlaps the gathers of step k+1)
             // crossing point weights: apex |s(i,i+1)|, slot i |p_{i+1}|, slot i+1 |p_i|.
             // Selections are written as predicated moves (IMAD.MOV on the FMA
             // pipe) rather than FSELs: the ALU pipe is the walker's hot pipe.
@@ -396,27 +425,15 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
             // crossing may come out as -1e-16 R, which is harmless in the sum
             const double chord = (zout - zin) * F.scale;
             if (BACK) {
-                if (chord > 0.0) atomicAdd(acc + t, chord * (double)yv);
+                if (chord > 0.0) atomicAdd(acc + tcur, chord * (double)yv);
             } else {
-                sum = fma(chord, (double)mut, sum);
+                sum = fma(chord, (double)mcur, sum);
             }
             ++n_cross;
-            // exit through the face opposite slot i+2 (local index L in t)
-            const int j = selp(2, selp(0, 1, c1), c0);
-            const int L = (lp >> (2 * j)) & 3;
-            const int lo = selp(selp(ta.x, ta.z, L == 0), selp(tb.x, tb.z, L == 2), L < 2);
-            if (lo < 0) break;
-            if (--steps_left == 0) { ++n_stuck; break; }
-            const unsigned hi = (unsigned)selp(selp(ta.y, ta.w, L == 0), selp(tb.y, tb.w, L == 2), L < 2);
-            // local indices in the next tet: kept slots map through `map`, the
-            // dropped slot j receives the current apex (local index kin)
-            const bool d0 = j == 0, d1 = j == 1, d2 = j == 2;
-            const int s0 = selp(kin, lp & 3, d0);
-            const int s1 = selp(kin, (lp >> 2) & 3, d1);
-            const int s2 = selp(kin, (lp >> 4) & 3, d2);
-            lp = ((hi >> (2 * s0)) & 3) | (((hi >> (2 * s1)) & 3) << 2) | (((hi >> (2 * s2)) & 3) << 4);
-            t = lo >> 2;
-            kin = lo & 3;
+            if (!more) {
+                if (lo >= 0) ++n_stuck;
+                break;
+            }
             // the apex takes the dropped slot i+2 (cyclic order is preserved);
             // s_{i+1} <- -p_{i+1}, s_{i+2} <- p_i
             if (d0) { x0 = x3; y0 = y3; z0 = z3; id0 = iap; s20 = -p2; s01 = p1; }
