@@ -365,18 +365,22 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
             const double p2 = side2(x3, y3, x2, y2);
             // exit face (apex, slot i, slot i+1): the unique i with
             // sign p_i = -1 and sign p_{i+1} = +1
-            int sa, sb, i;
-            SIGN_OF(p0, id0, sa);
-            if (sa < 0) {
-                SIGN_OF(p1, id1, sb);
-                i = sb > 0 ? 0 : 1;
-                if (i == 1 && p2 < -F.tau) ++n_lost;   // (-,-,-) is impossible
-            } else {
-                SIGN_OF(p2, id2, sb);
-                i = sb < 0 ? 2 : 1;
-                if (i == 1 && p1 > F.tau) ++n_lost;    // (+,+,+) is impossible
+            // All three filters are evaluated in parallel (ILP); a sign that the
+            // filter cannot certify is decided exactly (rare branch).  With
+            // n_k = [sign p_k = -1]: i = 0 for (1,0,*), 1 for (*,1,0), 2 for
+            // (0,*,1); (0,0,0) and (1,1,1) cannot occur for an entering ray.
+            bool n0 = p0 < -F.tau, n1 = p1 < -F.tau, n2 = p2 < -F.tau;
+            const bool u0 = !n0 && !(p0 > F.tau), u1 = !n1 && !(p1 > F.tau),
+                       u2 = !n2 && !(p2 > F.tau);
+            if (u0 | u1 | u2) {
+                if (u0) { n0 = exact_side_ids(vtx, ang, beam, a, u, v, iap, id0) < 0; ++n_exact; }
+                if (u1) { n1 = exact_side_ids(vtx, ang, beam, a, u, v, iap, id1) < 0; ++n_exact; }
+                if (u2) { n2 = exact_side_ids(vtx, ang, beam, a, u, v, iap, id2) < 0; ++n_exact; }
             }
-            const bool c0 = i == 0, c1 = i == 1;
+            const bool c0 = n0 && !n1;            // p0 = -1, p1 = +1
+            const bool c1 = n1 && !n2 && !c0;     // p1 = -1, p2 = +1
+            const int i = c0 ? 0 : (c1 ? 1 : 2);
+            n_lost += (n0 == n1 && n1 == n2) ? 1u : 0u;
             // exit through the face opposite slot j = i+2 (local index L in t)
             const int j = selp(2, selp(0, 1, c1), c0);
             const int L = (lp >> (2 * j)) & 3;
@@ -453,164 +457,6 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
     if (lane == 0 && mx) atomicMax(stats + ST_MAXC, (unsigned long long)mx);
 }
 
-// Walker variant with the three face slots in SHARED memory (per-thread
-// structure of arrays): the exit face's slot data are read and the dropped
-// slot written with indexed LDS/STS instead of register selects / predicated
-// moves, which frees ~27 registers per thread.  Same arithmetic as
-// trace_kernel.
-#define SIGN_S(val, k, out)                                                                  \
-    do {                                                                                   \
-        out = (val) > F.tau ? 1 : ((val) < -F.tau ? -1 : 0);                               \
-        if (!out) { out = exact_side_ids(vtx, ang, beam, a, u, v, iap, s_id[k][me]); ++n_exact; } \
-    } while (0)
-
-template <bool BACK, int MINB>
-__global__ void __launch_bounds__(128, MINB) trace_smem_kernel(const int4* __restrict__ rec,
-                                                               const int4* __restrict__ tnode,
-                                                               const int4* __restrict__ vtx,
-                                                               const AngleGeom* __restrict__ ang,
-                                                               int beam, int nv, int nu, double rmax,
-                                                               double g, int max_steps,
-                                                               const int* __restrict__ entry,
-                                                               const float* __restrict__ mu,
-                                                               float* __restrict__ proj,
-                                                               const float* __restrict__ y,
-                                                               double* __restrict__ acc,
-                                                               unsigned long long* __restrict__ stats) {
-    __shared__ double2 s_xy[3][128];   // slot k: shear coordinates (x', y')
-    __shared__ double s_z[3][128];     // slot k: depth z'
-    __shared__ double s_sig[3][128];   // side(slot k, slot k+1), exact sign -1
-    __shared__ int s_id[3][128];       // slot k: vertex id
-    const int me = threadIdx.x;
-    const int tiles_u = (nu + 15) >> 4;
-    const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
-    const int a = blockIdx.y;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int u = bx * 16 + (w & 1) * 8 + (lane & 7);
-    const int v = by * 8 + (w >> 1) * 4 + (lane >> 3);
-    const bool valid = u < nu && v < nv;
-    const size_t rid = ((size_t)a * nv + v) * nu + u;
-    const int e = valid ? entry[rid] : -1;
-
-    unsigned n_cross = 0, n_exact = 0, n_lost = 0, n_stuck = 0;
-    double sum = 0.0;
-    if (e >= 0) {
-        const RayPts r = ray_points(ang[a], beam, u, v);
-        Frame F;
-        make_frame(r, rmax, g, F);
-        const float yv = BACK ? y[rid] : 0.f;
-        int t = e >> 2, kin = e & 3;
-        const int4 nodes = __ldg(tnode + t);
-        int id0, id1, id2, lp;
-        if (kin == 0)      { id0 = nodes.y; id1 = nodes.z; id2 = nodes.w; lp = 1 | 2 << 2 | 3 << 4; }
-        else if (kin == 1) { id0 = nodes.x; id1 = nodes.w; id2 = nodes.z; lp = 0 | 3 << 2 | 2 << 4; }
-        else if (kin == 2) { id0 = nodes.x; id1 = nodes.y; id2 = nodes.w; lp = 0 | 1 << 2 | 3 << 4; }
-        else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; lp = 0 | 2 << 2 | 1 << 4; }
-        int iap = sel4(nodes, kin);
-        double zin;
-        {
-            double x0, y0, z0, x1, y1, z1, x2, y2, z2;
-            xform(F, __ldg(vtx + id0), x0, y0, z0);
-            xform(F, __ldg(vtx + id1), x1, y1, z1);
-            xform(F, __ldg(vtx + id2), x2, y2, z2);
-            const double s01 = side2(x0, y0, x1, y1), s12 = side2(x1, y1, x2, y2),
-                         s20 = side2(x2, y2, x0, y0);
-            const double w0 = fabs(s12), w1 = fabs(s20), w2 = fabs(s01);
-            const double sw = w0 + w1 + w2;
-            zin = sw > 0 ? (w0 * z0 + w1 * z1 + w2 * z2) / sw : (z0 + z1 + z2) * (1.0 / 3.0);
-            s_xy[0][me] = make_double2(x0, y0); s_z[0][me] = z0; s_id[0][me] = id0; s_sig[0][me] = s01;
-            s_xy[1][me] = make_double2(x1, y1); s_z[1][me] = z1; s_id[1][me] = id1; s_sig[1][me] = s12;
-            s_xy[2][me] = make_double2(x2, y2); s_z[2][me] = z2; s_id[2][me] = id2; s_sig[2][me] = s20;
-        }
-        int steps_left = max_steps;
-        int4 ta = ldg_nc_v4(rec + 2 * (size_t)t);
-        int4 tb = ldg_nc_v4(rec + 2 * (size_t)t + 1);
-        float mut = 0.f;
-        if (!BACK) mut = __ldg(mu + t);
-        int4 X = __ldg(vtx + iap);
-        while (true) {
-            const double2 q0 = s_xy[0][me], q1 = s_xy[1][me], q2 = s_xy[2][me];
-            double x3, y3, z3;
-            xform(F, X, x3, y3, z3);
-            const double p0 = side2(x3, y3, q0.x, q0.y);
-            const double p1 = side2(x3, y3, q1.x, q1.y);
-            const double p2 = side2(x3, y3, q2.x, q2.y);
-            int sa, sb, i;
-            SIGN_S(p0, 0, sa);
-            if (sa < 0) {
-                SIGN_S(p1, 1, sb);
-                i = sb > 0 ? 0 : 1;
-                if (i == 1 && p2 < -F.tau) ++n_lost;
-            } else {
-                SIGN_S(p2, 2, sb);
-                i = sb < 0 ? 2 : 1;
-                if (i == 1 && p1 > F.tau) ++n_lost;
-            }
-            const int in = selp(0, i + 1, i == 2);   // slot i+1
-            const int j = selp(2, i - 1, i == 0);    // slot i+2 (dropped)
-            const int L = (lp >> (2 * j)) & 3;
-            const int lo = selp(selp(ta.x, ta.z, L == 0), selp(tb.x, tb.z, L == 2), L < 2);
-            const unsigned hi = (unsigned)selp(selp(ta.y, ta.w, L == 0), selp(tb.y, tb.w, L == 2), L < 2);
-            const bool more = lo >= 0 && --steps_left != 0;
-            const int tcur = t;
-            const float mcur = mut;
-            if (more) {
-                t = lo >> 2;
-                ta = ldg_nc_v4(rec + 2 * (size_t)t);
-                tb = ldg_nc_v4(rec + 2 * (size_t)t + 1);
-                if (!BACK) mut = __ldg(mu + t);
-                X = __ldg(vtx + (int)(hi >> 8));
-                const int s0 = selp(kin, lp & 3, j == 0);
-                const int s1 = selp(kin, (lp >> 2) & 3, j == 1);
-                const int s2 = selp(kin, (lp >> 4) & 3, j == 2);
-                lp = ((hi >> (2 * s0)) & 3) | (((hi >> (2 * s1)) & 3) << 2) |
-                     (((hi >> (2 * s2)) & 3) << 4);
-                kin = lo & 3;
-            }
-            double pi = p2, pn = p0;
-            if (i == 0) { pi = p0; pn = p1; }
-            if (i == 1) { pi = p1; pn = p2; }
-            const double si = s_sig[i][me], zi = s_z[i][me], zn = s_z[in][me];
-            const double wA = fabs(si), wQ = fabs(pn), wR = fabs(pi);
-            const double sw = wA + wQ + wR;
-            double zout;
-            if (sw > 0.0) {
-                zout = fma(fma(wQ, zi - z3, wR * (zn - z3)), rcp_nr(sw), z3);
-            } else {
-                zout = zin;
-                ++n_exact;
-            }
-            const double chord = (zout - zin) * F.scale;
-            if (BACK) {
-                if (chord > 0.0) atomicAdd(acc + tcur, chord * (double)yv);
-            } else {
-                sum = fma(chord, (double)mcur, sum);
-            }
-            ++n_cross;
-            if (!more) {
-                if (lo >= 0) ++n_stuck;
-                break;
-            }
-            // the apex takes slot i+2; s_{i+1} <- -p_{i+1}, s_{i+2} <- p_i
-            s_xy[j][me] = make_double2(x3, y3);
-            s_z[j][me] = z3;
-            s_id[j][me] = iap;
-            s_sig[in][me] = -pn;
-            s_sig[j][me] = pi;
-            zin = zout;
-            iap = (int)(hi >> 8);
-        }
-    }
-    if (!BACK && valid) proj[rid] = (float)sum;
-    add_stat(stats, ST_HIT, e >= 0 ? 1u : 0u);
-    add_stat(stats, ST_CROSS, n_cross);
-    add_stat(stats, ST_EXACT, n_exact);
-    add_stat(stats, ST_LOST, n_lost);
-    add_stat(stats, ST_STUCK, n_stuck);
-    const unsigned mx = __reduce_max_sync(0xffffffffu, n_cross);
-    if (lane == 0 && mx) atomicMax(stats + ST_MAXC, (unsigned long long)mx);
-}
-
 // ------------------------------------------------------------ permute ---
 __global__ void gather_mu_kernel(const int* __restrict__ perm, const float* __restrict__ mu,
                                  float* __restrict__ out, int64_t n) {
@@ -654,46 +500,18 @@ static dim3 trace_grid(const LaunchChunk& c) {
     return dim3(tiles, (unsigned)c.n_angles);
 }
 
-// Resident blocks per SM requested from ptxas (register cap 65536/(128*MINB));
-// TETPROJ_MINB overrides the default for measurements.
-static int trace_minb() {
-    static int v = [] {
-        const char* e = getenv("TETPROJ_MINB");
-        const int x = e ? atoi(e) : 4;
-        return (x == 5 || x == 6) ? x : 4;
-    }();
-    return v;
-}
-
-// Walker slot storage (measurement knob): TETPROJ_SLOTS=smem selects
-// trace_smem_kernel, anything else the register-slot trace_kernel.
-static bool slots_in_smem() {
-    static int v = [] {
-        const char* e = getenv("TETPROJ_SLOTS");
-        return (e && e[0] == 's') ? 1 : 0;
-    }();
-    return v != 0;
-}
-
 #define TRACE_ARGS m.rec, m.tnode, m.vtx, c.ang, c.beam, c.nv, c.nu, m.rmax, m.g, steps, entry, \
                    mu_int, proj, y, acc, stats
 
+// 4 resident 128-thread blocks per SM (128 registers, no spills).  Capping the
+// registers for 5 or 6 blocks spills inside the loop and was measured slower
+// (DESIGN.md §5).
 template <bool BACK>
 static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entry,
                          const float* mu_int, float* proj, const float* y, double* acc,
                          unsigned long long* stats, cudaStream_t s) {
     const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
-    const dim3 grid = trace_grid(c);
-    const int mb = trace_minb();
-    if (slots_in_smem()) {
-        if (mb == 5) trace_smem_kernel<BACK, 5><<<grid, 128, 0, s>>>(TRACE_ARGS);
-        else if (mb == 6) trace_smem_kernel<BACK, 6><<<grid, 128, 0, s>>>(TRACE_ARGS);
-        else trace_smem_kernel<BACK, 4><<<grid, 128, 0, s>>>(TRACE_ARGS);
-    } else {
-        if (mb == 5) trace_kernel<BACK, 5><<<grid, 128, 0, s>>>(TRACE_ARGS);
-        else if (mb == 6) trace_kernel<BACK, 6><<<grid, 128, 0, s>>>(TRACE_ARGS);
-        else trace_kernel<BACK, 4><<<grid, 128, 0, s>>>(TRACE_ARGS);
-    }
+    trace_kernel<BACK, 4><<<trace_grid(c), 128, 0, s>>>(TRACE_ARGS);
 }
 
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
