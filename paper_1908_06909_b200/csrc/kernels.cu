@@ -163,7 +163,14 @@ __device__ __forceinline__ int sel4(int4 v, int k) {
 }
 
 __device__ __forceinline__ int4 ldg_nc_v4(const int4* p) {
-    return __ldg(p);  // ld.global.nc.v4: one 16-B request per record half
+    return __ldg(p);  // ld.global.nc.v4: one 16-B request
+}
+
+// One 256-bit request (LDG.E.ENL2.256 on sm_100a) for a 32-B face-tag record.
+__device__ __forceinline__ void ldg_rec256(const int4* p, int4& a, int4& b) {
+    asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+        : "l"(p));
 }
 
 // warp-aggregated stats
@@ -352,8 +359,8 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
         // the next tet, its apex vertex, mu) are issued as soon as step k's
         // exit face is known, and step k's chord / accumulation / slot update
         // run while they are in flight.
-        int4 ta = ldg_nc_v4(rec + 2 * (size_t)t);          // face tags of t (32 B)
-        int4 tb = ldg_nc_v4(rec + 2 * (size_t)t + 1);
+        int4 ta, tb;
+        ldg_rec256(rec + 2 * (size_t)t, ta, tb);             // face tags of t (32 B)
         float mut = 0.f;
         if (!BACK) mut = __ldg(mu + t);
         int4 X = __ldg(vtx + iap);                          // apex vertex (16 B)
@@ -392,8 +399,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
             const bool d0 = j == 0, d1 = j == 1, d2 = j == 2;
             if (more) {
                 t = lo >> 2;
-                ta = ldg_nc_v4(rec + 2 * (size_t)t);
-                tb = ldg_nc_v4(rec + 2 * (size_t)t + 1);
+                ldg_rec256(rec + 2 * (size_t)t, ta, tb);
                 if (!BACK) mut = __ldg(mu + t);
                 X = __ldg(vtx + (int)(hi >> 8));
                 // local indices in the next tet: kept slots map through `map`,
