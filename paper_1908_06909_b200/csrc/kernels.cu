@@ -296,20 +296,14 @@ __global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ tno
         if (!out) { out = exact_side_ids(vtx, ang, beam, a, u, v, iap, id_other); ++n_exact; } \
     } while (0)
 
-// kFace[k][p] (outward face order) packed 2 bits per entry at 2*(3k+p).
-constexpr unsigned kFaceLut = (1u << 0) | (2u << 2) | (3u << 4) |       // k = 0: 1 2 3
-                              (0u << 6) | (3u << 8) | (2u << 10) |      // k = 1: 0 3 2
-                              (0u << 12) | (1u << 14) | (3u << 16) |    // k = 2: 0 1 3
-                              (0u << 18) | (2u << 20) | (1u << 22);     // k = 3: 0 2 1
-
 // One thread per ray, 8x4-pixel warp tiles (16x8 per block).
 // State: the entry face in three fixed slots k = 0,1,2 in cyclic order (shear
-// coordinates x', y', z', vertex id; slot s = node kFace[kin][(s+rot)%3]) with
+// coordinates x', y', z', vertex id, local index l_k in the current tet) with
 // the edge sides s01, s12, s20 (exact sign -1), the apex id `iap` (from the
 // previous face tag), the entry depth zin.  Per step the face tags of t and
 // the apex vertex are gathered IN PARALLEL (the tag carried the apex id);
-// the tag of the exit face gives the next tet, its apex and the slot rotation,
-// so the neighbour's node list is never loaded.
+// the tag of the exit face gives the next tet, its apex and the local-index
+// map, so the neighbour's node list is never loaded.
 template <bool BACK, int MINB>
 __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict__ rec,
                                                           const int4* __restrict__ tnode,
@@ -343,12 +337,11 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
         int t = e >> 2, kin = e & 3;
         const int4 nodes = __ldg(tnode + t);
         // entry face = face kin in outward order (opposite node kin)
-        // slot s holds node kFace[kin][(s + rot) % 3] of the current tet
-        int id0, id1, id2, rot = 0;
-        if (kin == 0)      { id0 = nodes.y; id1 = nodes.z; id2 = nodes.w; }
-        else if (kin == 1) { id0 = nodes.x; id1 = nodes.w; id2 = nodes.z; }
-        else if (kin == 2) { id0 = nodes.x; id1 = nodes.y; id2 = nodes.w; }
-        else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; }
+        int id0, id1, id2, lp;
+        if (kin == 0)      { id0 = nodes.y; id1 = nodes.z; id2 = nodes.w; lp = 1 | 2 << 2 | 3 << 4; }
+        else if (kin == 1) { id0 = nodes.x; id1 = nodes.w; id2 = nodes.z; lp = 0 | 3 << 2 | 2 << 4; }
+        else if (kin == 2) { id0 = nodes.x; id1 = nodes.y; id2 = nodes.w; lp = 0 | 1 << 2 | 3 << 4; }
+        else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; lp = 0 | 2 << 2 | 1 << 4; }
         int iap = sel4(nodes, kin);
         double x0, y0, z0, x1, y1, z1, x2, y2, z2;
         xform(F, __ldg(vtx + id0), x0, y0, z0);
@@ -397,9 +390,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
             n_lost += (n0 == n1 && n1 == n2) ? 1u : 0u;
             // exit through the face opposite slot j = i+2 (local index L in t)
             const int j = selp(2, selp(0, 1, c1), c0);
-            int q = j + rot;
-            q = selp(q - 3, q, q >= 3);
-            const int L = (kFaceLut >> (2 * (3 * kin + q))) & 3;
+            const int L = (lp >> (2 * j)) & 3;
             const int lo = selp(selp(ta.x, ta.z, L == 0), selp(tb.x, tb.z, L == 2), L < 2);
             const unsigned hi = (unsigned)selp(selp(ta.y, ta.w, L == 0), selp(tb.y, tb.w, L == 2), L < 2);
             const bool more = lo >= 0 && --steps_left != 0;
@@ -411,11 +402,13 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
                 ldg_rec256(rec + 2 * (size_t)t, ta, tb);
                 if (!BACK) mut = __ldg(mu + t);
                 X = __ldg(vtx + (int)(hi >> 8));
-                // slot j receives the current apex (node kin of t), found at
-                // position pos of the next tet's face order: rot' = pos - j mod 3
-                const int pos = (hi >> (2 * kin)) & 3;
-                rot = pos - j;
-                rot = selp(rot + 3, rot, rot < 0);
+                // local indices in the next tet: kept slots map through `map`,
+                // the dropped slot j receives the current apex (local index kin)
+                const int s0 = selp(kin, lp & 3, d0);
+                const int s1 = selp(kin, (lp >> 2) & 3, d1);
+                const int s2 = selp(kin, (lp >> 4) & 3, d2);
+                lp = ((hi >> (2 * s0)) & 3) | (((hi >> (2 * s1)) & 3) << 2) |
+                     (((hi >> (2 * s2)) & 3) << 4);
                 kin = lo & 3;
             }
             // ---- chord of step k (overlaps the gathers of step k+1)

@@ -282,13 +282,11 @@ tet_status prepare_mesh(const double* verts, int64_t nv, const int32_t* tets,
     // Face tags: face k of tet t -> two int32 words
     //   lo = n<<2 | k'            (n = neighbour, k' = shared face's local index
     //                              in n = local index of n's apex); -1 on the hull
-    //   hi = apex<<8 | pos        (apex = vertex id of node k' of n; pos holds,
-    //                              2 bits per t-local index j != k, the position
-    //                              of node j of t in n's outward face order
-    //                              kFace[k'] -- the walker's slots are always a
-    //                              cyclic rotation of that order)
-    // so the walker gets the next apex and its slot rotation without loading
-    // the neighbour's node list.
+    //   hi = apex<<8 | map        (apex = vertex id of node k' of n; map holds,
+    //                              2 bits per t-local index j != k, the n-local
+    //                              index of node j of t)
+    // so the walker gets the next apex and the slots' local indices without
+    // loading the neighbour's node list.
     if (nvu > (1 << 23)) { err = "more than 2^23 vertices (face-tag apex field)"; return TET_E_MESH; }
     M.rec.assign((size_t)nt * 8, 0);
     M.tnode.assign((size_t)nt * 4, 0);
@@ -308,11 +306,10 @@ tet_status prepare_mesh(const double* verts, int64_t nv, const int32_t* tets,
             uint32_t map = 0;
             for (int j = 0; j < 4; ++j) {
                 if (j == k) continue;
-                int pos = -1;
-                for (int p = 0; p < 3; ++p)
-                    if (T[4 * (int64_t)n + kFace[kp][p]] == T[4 * t + j]) pos = p;
-                if (pos < 0) { err = "internal: shared face mismatch"; return TET_E_MESH; }
-                map |= (uint32_t)pos << (2 * j);
+                int m = -1;
+                for (int jj = 0; jj < 4; ++jj)
+                    if (T[4 * (int64_t)n + jj] == T[4 * t + j]) m = jj;
+                map |= (uint32_t)m << (2 * j);
             }
             const uint32_t apex = (uint32_t)vnew[T[4 * (int64_t)n + kp]];
             M.rec[8 * i + 2 * k] = (inv[n] << 2) | kp;
