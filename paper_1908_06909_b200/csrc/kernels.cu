@@ -365,16 +365,6 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
         if (!BACK) mut = __ldg(mu + t);
         int4 X = __ldg(vtx + iap);                          // apex vertex (16 B)
         while (true) {
-            // Candidate exit tags, one per slot k (exit opposite slot k = face
-            // local index l_k): selected while the apex transform is in flight,
-            // so only a 2-level select remains after the exit decision.
-            const int l0 = lp & 3, l1 = (lp >> 2) & 3, l2 = (lp >> 4) & 3;
-            const int lo0 = selp(selp(ta.x, ta.z, l0 == 0), selp(tb.x, tb.z, l0 == 2), l0 < 2);
-            const int lo1 = selp(selp(ta.x, ta.z, l1 == 0), selp(tb.x, tb.z, l1 == 2), l1 < 2);
-            const int lo2 = selp(selp(ta.x, ta.z, l2 == 0), selp(tb.x, tb.z, l2 == 2), l2 < 2);
-            const int hi0 = selp(selp(ta.y, ta.w, l0 == 0), selp(tb.y, tb.w, l0 == 2), l0 < 2);
-            const int hi1 = selp(selp(ta.y, ta.w, l1 == 0), selp(tb.y, tb.w, l1 == 2), l1 < 2);
-            const int hi2 = selp(selp(ta.y, ta.w, l2 == 0), selp(tb.y, tb.w, l2 == 2), l2 < 2);
             double x3, y3, z3;
             xform(F, X, x3, y3, z3);
             const double p0 = side2(x3, y3, x0, y0);   // side(apex, slot k)
@@ -398,10 +388,11 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
             const bool c1 = n1 && !n2 && !c0;     // p1 = -1, p2 = +1
             const int i = c0 ? 0 : (c1 ? 1 : 2);
             n_lost += (n0 == n1 && n1 == n2) ? 1u : 0u;
-            // exit through the face opposite slot j = i+2
+            // exit through the face opposite slot j = i+2 (local index L in t)
             const int j = selp(2, selp(0, 1, c1), c0);
-            const int lo = selp(lo2, selp(lo0, lo1, c1), c0);
-            const unsigned hi = (unsigned)selp(hi2, selp(hi0, hi1, c1), c0);
+            const int L = (lp >> (2 * j)) & 3;
+            const int lo = selp(selp(ta.x, ta.z, L == 0), selp(tb.x, tb.z, L == 2), L < 2);
+            const unsigned hi = (unsigned)selp(selp(ta.y, ta.w, L == 0), selp(tb.y, tb.w, L == 2), L < 2);
             const bool more = lo >= 0 && --steps_left != 0;
             const int tcur = t;
             const float mcur = mut;
