@@ -136,24 +136,29 @@ def ncu_traffic(kernel, crossings_per_launch):
         return None
 
 
-def cpu_baseline(w, geom, y, budget_angles=12):
-    """The oracle as it stands, on this host's cores, on a bounded sample:
-    `budget_angles` evenly spaced angles of the rank-0 scan, all pixels."""
+def cpu_baseline(w, geom, y, budget_s=15.0):
+    """The oracle as it stands, on this host's cores, on a bounded sample of
+    the same scan: an evenly strided subset of ray ids (all angles), sized
+    from a short calibration run to ~budget_s seconds of fwd+back work."""
     from oracle import tetref as O
-    idx = np.linspace(0, geom.n_angles - 1, budget_angles).round().astype(int)
-    sub = geom.subset(idx)
     om = O.OracleMesh.from_mesh(w.mesh)
     cores = len(os.sched_getaffinity(0))
-    ysub = y[idx]
-    t0 = time.perf_counter()
-    _, st = O.project(om, sub, w.mu.astype(np.float64), nthreads=cores)
-    _, st2 = O.backproject(om, sub, ysub, nthreads=cores)
-    dt = time.perf_counter() - t0
-    cross = st["crossings"] + st2["crossings"]
+    mu = w.mu.astype(np.float64)
+    yflat = y.reshape(-1)
+
+    def run(n):
+        ids = np.linspace(0, geom.n_rays - 1, n).round().astype(np.int64)
+        t0 = time.perf_counter()
+        _, st = O.project(om, geom, mu, ray_ids=ids, nthreads=cores)
+        _, st2 = O.backproject(om, geom, yflat[ids], ray_ids=ids, nthreads=cores)
+        return time.perf_counter() - t0, st["crossings"] + st2["crossings"], n
+
+    dt, cross, n = run(20000)
+    n2 = int(min(geom.n_rays, max(20000, 20000 * budget_s / max(dt, 1e-3))))
+    dt, cross, n = run(n2)
     return {"value": cross / dt, "unit": "tet-crossings/s", "cores": cores, "kind": "oracle",
-            "sample": f"{budget_angles} of {geom.n_angles} angles (evenly spaced), all "
-                      f"{sub.n_v}x{sub.n_u} pixels, fwd+back, {dt:.1f} s",
-            "crossings": cross, "seconds": dt}
+            "sample": f"{n} of {geom.n_rays} rays (evenly strided over all angles), "
+                      f"fwd+back, {dt:.1f} s", "crossings": int(cross), "seconds": dt}
 
 
 def run_reference(args):
