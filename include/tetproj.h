@@ -88,7 +88,28 @@ typedef struct {
     uint64_t entry_conflicts;   /* pixels claimed by >1 hull face (must be 0)    */
     uint32_t max_crossings_per_ray;
     uint32_t _pad;
+    uint64_t escalations;       /* paper-faithful modes: epsilon escalations      */
 } tet_stats;
+
+/* Traversal mode (tet_project_ex / tet_backproject_ex).
+ *   TET_TRAVERSE_EXACT  : exact Plücker signs + SoS (default; R2-R5)
+ *   TET_TRAVERSE_MT_F64 : the paper's Alg. 1 (Möller-Trumbore with safety
+ *                         parameter eps) inside Alg. 2 (eps
+ *                         escalation x eps_growth until two faces are hit,
+ *                         swap check on zero-length steps)
+ *                         in double precision on world coordinates
+ *   TET_TRAVERSE_MT_F32 : the same in single precision (the failure mode of
+ *                         fig:singledouble)
+ * The MT modes exist to reproduce the paper's robustness study: rays whose
+ * escalation exceeds max_escalations are counted as `lost` and contribute what
+ * was summed so far; walks longer than n_tets steps are `stuck`.             */
+enum { TET_TRAVERSE_EXACT = 0, TET_TRAVERSE_MT_F64 = 1, TET_TRAVERSE_MT_F32 = 2 };
+typedef struct {
+    int32_t traversal;         /* TET_TRAVERSE_*                                 */
+    int32_t max_escalations;   /* MT modes: 12 (SPEC.md:314 reading)            */
+    double eps0;               /* MT modes: 1e-9 ("eps <- 10^-9")  */
+    double eps_growth;         /* MT modes: 10 ("eps <- eps*10")   */
+} tet_options;
 
 /* Create a mesh on CUDA device `device` (§2.2 graph + boundary list).
  *   verts  [n_verts][3] double   world coordinates (host)
@@ -127,6 +148,13 @@ tet_status tet_backproject(tet_mesh_t m, const tet_geometry* g, const float* pro
  * driver to all-reduce double partial sums.                                  */
 tet_status tet_backproject_f64(tet_mesh_t m, const tet_geometry* g, const float* proj,
                                double* acc, void* cuda_stream, tet_stats* st);
+
+/* tet_project / tet_backproject with traversal options (NULL = exact). */
+tet_status tet_project_ex(tet_mesh_t m, const tet_geometry* g, const float* mu, float* proj,
+                          const tet_options* opt, void* cuda_stream, tet_stats* st);
+tet_status tet_backproject_ex(tet_mesh_t m, const tet_geometry* g, const float* proj, float* x,
+                              int accumulate, const tet_options* opt, void* cuda_stream,
+                              tet_stats* st);
 
 /* Introspection (for tests / bench).  info[0..7] = n_verts, n_tets, n_bfaces,
  * device, grid exponent e (g = 2^e), bytes of device mesh data, L2 persisting

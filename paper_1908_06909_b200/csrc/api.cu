@@ -146,8 +146,19 @@ struct KernelTimer {
 
 // Shared driver: geometry prep, chunking over angles, entry finder, walker.
 tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, int accumulate,
-               Op op, void* stream, tet_stats* st) {
+               Op op, void* stream, tet_stats* st, const tet_options* opt = nullptr) {
     if (!m) return fail(TET_E_ARG, "null mesh");
+    const int mode = opt ? opt->traversal : TET_TRAVERSE_EXACT;
+    if (mode < TET_TRAVERSE_EXACT || mode > TET_TRAVERSE_MT_F32)
+        return fail(TET_E_ARG, "unknown traversal mode");
+    MtOptions mto;
+    if (opt && mode != TET_TRAVERSE_EXACT) {
+        if (!(opt->eps0 > 0) || !(opt->eps_growth > 1) || opt->max_escalations < 0)
+            return fail(TET_E_ARG, "bad MT options (eps0 > 0, eps_growth > 1, max_escalations >= 0)");
+        mto.eps0 = opt->eps0;
+        mto.eps_growth = opt->eps_growth;
+        mto.max_escalations = opt->max_escalations;
+    }
     if (!g || !in || !out) return fail(TET_E_ARG, "null argument");
     std::vector<AngleGeom> ang;
     std::vector<AngleAux> aux;
@@ -221,7 +232,12 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
             }
             const size_t off = (size_t)a0 * per_angle;
             const bool fwd = op == Op::Forward;
-            if (fwd) {
+            if (mode != TET_TRAVERSE_EXACT) {
+                KernelTimer kt(m, fwd ? TET_K_FORWARD : TET_K_BACKWARD, s);
+                CU(launch_mt(m->dev, c, !fwd, mode == TET_TRAVERSE_MT_F32, mto, entry, mu_int,
+                             fwd ? (float*)d_out + off : nullptr, fwd ? nullptr : d_in + off, acc,
+                             d_stats, s));
+            } else if (fwd) {
                 KernelTimer kt(m, TET_K_FORWARD, s);
                 CU(launch_forward(m->dev, c, entry, mu_int, (float*)d_out + off, d_stats, s));
             } else {
@@ -253,6 +269,7 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         st->exact_fallbacks = hs[ST_EXACT];
         st->entry_conflicts = hs[ST_CONFLICT];
         st->max_crossings_per_ray = (uint32_t)hs[ST_MAXC];
+        st->escalations = hs[ST_ESC];
     }
     if (strict && (hs[ST_LOST] || hs[ST_STUCK] || hs[ST_CONFLICT]))
         return fail(TET_E_RAYS, "lost / stuck / conflicting rays (TET_F_STRICT)");
@@ -312,6 +329,7 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     m->dev.nb = H.nb;
     m->dev.g = H.g;
     m->dev.rmax = H.rmax;
+    for (int i = 0; i < 3; ++i) m->dev.C[i] = H.C[i];
     // host copies are no longer needed
     std::vector<int32_t>().swap(H.rec);
     std::vector<int32_t>().swap(H.tnode);
@@ -342,6 +360,17 @@ tet_status tet_mesh_destroy(tet_mesh_t m) {
 tet_status tet_project(tet_mesh_t m, const tet_geometry* g, const float* mu, float* proj,
                        void* cuda_stream, tet_stats* st) {
     return run(m, g, mu, proj, 0, Op::Forward, cuda_stream, st);
+}
+
+tet_status tet_project_ex(tet_mesh_t m, const tet_geometry* g, const float* mu, float* proj,
+                          const tet_options* opt, void* cuda_stream, tet_stats* st) {
+    return run(m, g, mu, proj, 0, Op::Forward, cuda_stream, st, opt);
+}
+
+tet_status tet_backproject_ex(tet_mesh_t m, const tet_geometry* g, const float* proj, float* x,
+                              int accumulate, const tet_options* opt, void* cuda_stream,
+                              tet_stats* st) {
+    return run(m, g, proj, x, accumulate, Op::Backward, cuda_stream, st, opt);
 }
 
 tet_status tet_backproject(tet_mesh_t m, const tet_geometry* g, const float* proj, float* x,

@@ -64,10 +64,16 @@ struct DevMesh {
     const int* perm = nullptr;   // [T]
     int64_t nv = 0, nt = 0, nb = 0;
     double g = 0, rmax = 0;
+    double C[3] = {0, 0, 0};     // grid origin (world units)
+};
+
+struct MtOptions {
+    double eps0 = 1e-9, eps_growth = 10.0;
+    int max_escalations = 12;
 };
 
 enum StatSlot {
-    ST_RAYS = 0, ST_HIT, ST_CROSS, ST_LOST, ST_STUCK, ST_EXACT, ST_CONFLICT, ST_MAXC,
+    ST_RAYS = 0, ST_HIT, ST_CROSS, ST_LOST, ST_STUCK, ST_EXACT, ST_CONFLICT, ST_MAXC, ST_ESC,
     ST_COUNT
 };
 
@@ -86,6 +92,9 @@ cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* en
 cudaError_t launch_backward(const DevMesh& m, const LaunchChunk& c, const int* entry,
                             const float* y, double* acc, unsigned long long* stats,
                             cudaStream_t s);
+cudaError_t launch_mt(const DevMesh& m, const LaunchChunk& c, bool back, bool single,
+                      const MtOptions& o, const int* entry, const float* mu_int, float* proj,
+                      const float* y, double* acc, unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_gather_mu(const DevMesh& m, const float* mu, float* mu_int,
                              cudaStream_t s);
 cudaError_t launch_scatter_x(const DevMesh& m, const double* acc, float* x, int accumulate,

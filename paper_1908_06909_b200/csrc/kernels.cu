@@ -386,7 +386,6 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
             }
             const bool c0 = n0 && !n1;            // p0 = -1, p1 = +1
             const bool c1 = n1 && !n2 && !c0;     // p1 = -1, p2 = +1
-            const int i = c0 ? 0 : (c1 ? 1 : 2);
             n_lost += (n0 == n1 && n1 == n2) ? 1u : 0u;
             // exit through the face opposite slot j = i+2 (local index L in t)
             const int j = selp(2, selp(0, 1, c1), c0);
@@ -461,6 +460,155 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
     add_stat(stats, ST_STUCK, n_stuck);
     const unsigned mx = __reduce_max_sync(0xffffffffu, n_cross);
     if (lane == 0 && mx) atomicMax(stats + ST_MAXC, (unsigned long long)mx);
+}
+
+// ------------------------------------------- paper-faithful walker ------
+// NEXT-1: the paper's own traversal, kept verbatim to measure
+// the robustness gap -- Alg. 1 "Möller Trumbore with safety parameter eps"
+// and Alg. 2 in precision T on world
+// coordinates.  The first tet comes from the exact entry map (the paper's
+// R*-tree initialisation is replaced); everything after it is
+// the paper's method, including its failure modes.
+template <class T>
+__device__ __forceinline__ bool mt_hit(const T r1[3], const T d[3], const T p1[3], const T p2[3],
+                                       const T p3[3], T eps, T& t) {
+    const T e1[3] = {p2[0] - p1[0], p2[1] - p1[1], p2[2] - p1[2]};
+    const T e2[3] = {p3[0] - p1[0], p3[1] - p1[1], p3[2] - p1[2]};
+    const T q[3] = {d[1] * e2[2] - d[2] * e2[1], d[2] * e2[0] - d[0] * e2[2],
+                    d[0] * e2[1] - d[1] * e2[0]};
+    const T a = e1[0] * q[0] + e1[1] * q[1] + e1[2] * q[2];
+    if (a > T(-1e-8) && a < T(1e-8)) return false;            // "Check if its zero"
+    const T f = T(1) / a;
+    const T s[3] = {r1[0] - p1[0], r1[1] - p1[1], r1[2] - p1[2]};
+    const T u = f * (s[0] * q[0] + s[1] * q[1] + s[2] * q[2]);
+    if (u < -eps) return false;
+    const T r[3] = {s[1] * e1[2] - s[2] * e1[1], s[2] * e1[0] - s[0] * e1[2],
+                    s[0] * e1[1] - s[1] * e1[0]};
+    const T v = f * (d[0] * r[0] + d[1] * r[1] + d[2] * r[2]);   // printed "d x r": a dot (R2 reading)
+    if (v < -eps || u + v > T(1) + eps) return false;
+    t = f * (e2[0] * r[0] + e2[1] * r[1] + e2[2] * r[2]);
+    return true;
+}
+
+template <class T>
+__device__ __forceinline__ void world_vertex(const int4* __restrict__ vtx, int id, double g,
+                                             const double C[3], T out[3]) {
+    const int4 X = __ldg(vtx + id);
+    out[0] = (T)fma((double)X.x, g, C[0]);
+    out[1] = (T)fma((double)X.y, g, C[1]);
+    out[2] = (T)fma((double)X.z, g, C[2]);
+}
+
+template <class T, bool BACK>
+__global__ void __launch_bounds__(128) mt_trace_kernel(const int4* __restrict__ rec,
+                                                       const int4* __restrict__ tnode,
+                                                       const int4* __restrict__ vtx,
+                                                       const AngleGeom* __restrict__ ang,
+                                                       int beam, int nv, int nu, double g,
+                                                       double cx, double cy, double cz,
+                                                       int max_steps, double eps0,
+                                                       double eps_growth, int max_esc,
+                                                       const int* __restrict__ entry,
+                                                       const float* __restrict__ mu,
+                                                       float* __restrict__ proj,
+                                                       const float* __restrict__ y,
+                                                       double* __restrict__ acc,
+                                                       unsigned long long* __restrict__ stats) {
+    const int tiles_u = (nu + 15) >> 4;
+    const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
+    const int a = blockIdx.y;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int u = bx * 16 + (w & 1) * 8 + (lane & 7);
+    const int v = by * 8 + (w >> 1) * 4 + (lane >> 3);
+    const bool valid = u < nu && v < nv;
+    const size_t rid = ((size_t)a * nv + v) * nu + u;
+    const int e = valid ? entry[rid] : -1;
+    const double C[3] = {cx, cy, cz};
+    unsigned n_cross = 0, n_lost = 0, n_stuck = 0, n_esc = 0;
+    double sum = 0.0;
+    if (e >= 0) {
+        const RayPts rp = ray_points(ang[a], beam, u, v);
+        const double R1d[3] = {fma((double)rp.ox, g, C[0]), fma((double)rp.oy, g, C[1]),
+                               fma((double)rp.oz, g, C[2])};
+        const double R2d[3] = {fma((double)rp.px, g, C[0]), fma((double)rp.py, g, C[1]),
+                               fma((double)rp.pz, g, C[2])};
+        const T R1[3] = {(T)R1d[0], (T)R1d[1], (T)R1d[2]};
+        const T R2[3] = {(T)R2d[0], (T)R2d[1], (T)R2d[2]};
+        const T d[3] = {R2[0] - R1[0], R2[1] - R1[1], R2[2] - R1[2]};
+        const T l = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);   // l = ||R2 - R1||
+        const float yv = BACK ? y[rid] : 0.f;
+        int t = e >> 2, prev = -1;
+        int steps = 0;
+        while (t >= 0) {
+            const int4 nd = __ldg(tnode + t);
+            const int ids[4] = {nd.x, nd.y, nd.z, nd.w};
+            T P[4][3];
+            for (int k = 0; k < 4; ++k) world_vertex<T>(vtx, ids[k], g, C, P[k]);
+            // while not Intersection: TetraRayIntersection(i_now, eps); eps *= 10
+            T eps = (T)eps0;
+            int esc = 0, nhit = 0, kmin = -1, kmax = -1;
+            T tmin = 0, tmax = 0;
+            while (true) {
+                nhit = 0;
+                for (int k = 0; k < 4; ++k) {   // the face opposite node k
+                    const int i0 = k == 0 ? 1 : 0, i1 = k <= 1 ? 2 : 1, i2 = k <= 2 ? 3 : 2;
+                    T th;
+                    if (mt_hit<T>(R1, d, P[i0], P[i1], P[i2], eps, th)) {
+                        if (nhit == 0 || th < tmin) { tmin = th; kmin = k; }
+                        if (nhit == 0 || th > tmax) { tmax = th; kmax = k; }
+                        ++nhit;
+                    }
+                }
+                if (nhit >= 2 || esc >= max_esc) break;
+                eps = eps * (T)eps_growth;
+                ++esc;
+            }
+            n_esc += esc;
+            if (nhit < 2) { ++n_lost; break; }                // the "black dots"
+            const double chord = (double)(l * (tmax - tmin));
+            if (BACK) {
+                if (chord > 0.0) atomicAdd(acc + t, chord * (double)yv);
+            } else {
+                sum = fma(chord, (double)__ldg(mu + t), sum);
+            }
+            ++n_cross;
+            // neighbour of the face where t2 happened; "if t2 = t1 check if they
+            // need to be swapped": do not step back into the previous element
+            const int4 r0 = __ldg(rec + 2 * (size_t)t), r1v = __ldg(rec + 2 * (size_t)t + 1);
+            const int nb[4] = {r0.x, r0.z, r1v.x, r1v.z};
+            int nxt = nb[kmax] < 0 ? -1 : (nb[kmax] >> 2);
+            if (tmax == tmin && nxt == prev && kmin != kmax) nxt = nb[kmin] < 0 ? -1 : (nb[kmin] >> 2);
+            prev = t;
+            t = nxt;
+            if (++steps >= max_steps) { ++n_stuck; break; }
+        }
+    }
+    if (!BACK && valid) proj[rid] = (float)sum;
+    add_stat(stats, ST_HIT, e >= 0 ? 1u : 0u);
+    add_stat(stats, ST_CROSS, n_cross);
+    add_stat(stats, ST_LOST, n_lost);
+    add_stat(stats, ST_STUCK, n_stuck);
+    add_stat(stats, ST_ESC, n_esc);
+    const unsigned mx = __reduce_max_sync(0xffffffffu, n_cross);
+    if (lane == 0 && mx) atomicMax(stats + ST_MAXC, (unsigned long long)mx);
+}
+
+cudaError_t launch_mt(const DevMesh& m, const LaunchChunk& c, bool back, bool single,
+                      const MtOptions& o, const int* entry, const float* mu_int, float* proj,
+                      const float* y, double* acc, unsigned long long* stats, cudaStream_t s) {
+    const dim3 grid(((c.nu + 15) / 16) * ((c.nv + 7) / 8), c.n_angles);
+    const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
+#define MT_ARGS m.rec, m.tnode, m.vtx, c.ang, c.beam, c.nv, c.nu, m.g, m.C[0], m.C[1], m.C[2], \
+                steps, o.eps0, o.eps_growth, o.max_escalations, entry, mu_int, proj, y, acc, stats
+    if (single) {
+        if (back) mt_trace_kernel<float, true><<<grid, 128, 0, s>>>(MT_ARGS);
+        else mt_trace_kernel<float, false><<<grid, 128, 0, s>>>(MT_ARGS);
+    } else {
+        if (back) mt_trace_kernel<double, true><<<grid, 128, 0, s>>>(MT_ARGS);
+        else mt_trace_kernel<double, false><<<grid, 128, 0, s>>>(MT_ARGS);
+    }
+#undef MT_ARGS
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------ permute ---

@@ -44,15 +44,29 @@ class tet_stats(C.Structure):
     _fields_ = [("rays", C.c_uint64), ("rays_hit", C.c_uint64), ("crossings", C.c_uint64),
                 ("lost", C.c_uint64), ("stuck", C.c_uint64), ("exact_fallbacks", C.c_uint64),
                 ("entry_conflicts", C.c_uint64), ("max_crossings_per_ray", C.c_uint32),
-                ("_pad", C.c_uint32)]
+                ("_pad", C.c_uint32), ("escalations", C.c_uint64)]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_ if k != "_pad"}
 
 
+TET_TRAVERSE_EXACT, TET_TRAVERSE_MT_F64, TET_TRAVERSE_MT_F32 = 0, 1, 2
+
+
+class tet_options(C.Structure):
+    _fields_ = [("traversal", C.c_int32), ("max_escalations", C.c_int32), ("eps0", C.c_double),
+                ("eps_growth", C.c_double)]
+
+
+def options(traversal: int = TET_TRAVERSE_EXACT, eps0: float = 1e-9, eps_growth: float = 10.0,
+            max_escalations: int = 12) -> tet_options:
+    """Traversal options; MT modes are the paper's Alg. 1/2."""
+    return tet_options(traversal, max_escalations, eps0, eps_growth)
+
+
 EXPORTS = ["tet_mesh_create", "tet_mesh_destroy", "tet_project", "tet_backproject",
            "tet_backproject_f64", "tet_mesh_info", "tet_last_error", "tet_set_kernel_timing",
-           "tet_kernel_times"]
+           "tet_kernel_times", "tet_project_ex", "tet_backproject_ex"]
 KERNEL_CLASSES = ["entry", "forward", "backward", "permute"]
 
 _lib = None
@@ -79,12 +93,16 @@ def lib(build: bool = False) -> C.CDLL:
     L.tet_backproject_f64.argtypes = [P, C.POINTER(tet_geometry), P, P, P,
                                       C.POINTER(tet_stats)]
     L.tet_mesh_info.argtypes = [P, C.POINTER(C.c_int64)]
+    L.tet_project_ex.argtypes = [P, C.POINTER(tet_geometry), P, P, C.POINTER(tet_options), P,
+                                 C.POINTER(tet_stats)]
+    L.tet_backproject_ex.argtypes = [P, C.POINTER(tet_geometry), P, P, C.c_int,
+                                     C.POINTER(tet_options), P, C.POINTER(tet_stats)]
     L.tet_set_kernel_timing.argtypes = [P, C.c_int]
     L.tet_kernel_times.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     L.tet_last_error.restype = C.c_char_p
     for f in ("tet_mesh_create", "tet_mesh_destroy", "tet_project", "tet_backproject",
               "tet_backproject_f64", "tet_mesh_info", "tet_set_kernel_timing",
-              "tet_kernel_times"):
+              "tet_kernel_times", "tet_project_ex", "tet_backproject_ex"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -193,26 +211,36 @@ def tet_kernel_times(m: MeshHandle) -> dict:
     return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(KERNEL_CLASSES)}
 
 
-def tet_project(m: MeshHandle, geom, mu, proj, stream=None, stats: bool = False):
+def tet_project(m: MeshHandle, geom, mu, proj, stream=None, stats: bool = False,
+                opts: tet_options | None = None):
     """proj = A mu (Eq. 2).  Returns the stats dict when ``stats``."""
     g, keep = _geom(geom)
     _, pmu = _ptr(mu, np.float32, m.n_tets)
     _, pp = _ptr(proj, np.float32, geom.n_angles * geom.n_v * geom.n_u)
     st = tet_stats()
-    _check(lib().tet_project(m.ptr, C.byref(g), pmu, pp, _stream(stream, mu, proj),
-                             C.byref(st) if stats else None))
+    sp = C.byref(st) if stats else None
+    if opts is None:
+        _check(lib().tet_project(m.ptr, C.byref(g), pmu, pp, _stream(stream, mu, proj), sp))
+    else:
+        _check(lib().tet_project_ex(m.ptr, C.byref(g), pmu, pp, C.byref(opts),
+                                    _stream(stream, mu, proj), sp))
     return st.as_dict() if stats else None
 
 
 def tet_backproject(m: MeshHandle, geom, proj, x, accumulate: bool = False, stream=None,
-                    stats: bool = False):
+                    stats: bool = False, opts: tet_options | None = None):
     """x = A^T proj (Eq. 3), or x += A^T proj."""
     g, keep = _geom(geom)
     _, pp = _ptr(proj, np.float32, geom.n_angles * geom.n_v * geom.n_u)
     _, px = _ptr(x, np.float32, m.n_tets)
     st = tet_stats()
-    _check(lib().tet_backproject(m.ptr, C.byref(g), pp, px, 1 if accumulate else 0,
-                                 _stream(stream, proj, x), C.byref(st) if stats else None))
+    sp = C.byref(st) if stats else None
+    if opts is None:
+        _check(lib().tet_backproject(m.ptr, C.byref(g), pp, px, 1 if accumulate else 0,
+                                     _stream(stream, proj, x), sp))
+    else:
+        _check(lib().tet_backproject_ex(m.ptr, C.byref(g), pp, px, 1 if accumulate else 0,
+                                        C.byref(opts), _stream(stream, proj, x), sp))
     return st.as_dict() if stats else None
 
 
@@ -246,18 +274,18 @@ class TetMesh:
     def info(self) -> dict:
         return tet_mesh_info(self.handle)
 
-    def project(self, geom, mu, out=None, stats: bool = False):
+    def project(self, geom, mu, out=None, stats: bool = False, opts=None):
         import torch
         if out is None:
             out = torch.empty((geom.n_angles, geom.n_v, geom.n_u), dtype=torch.float32,
                               device=mu.device if isinstance(mu, torch.Tensor) else "cpu")
-        st = tet_project(self.handle, geom, mu, out, stats=stats)
+        st = tet_project(self.handle, geom, mu, out, stats=stats, opts=opts)
         return (out, st) if stats else out
 
-    def backproject(self, geom, proj, out=None, accumulate=False, stats: bool = False):
+    def backproject(self, geom, proj, out=None, accumulate=False, stats: bool = False, opts=None):
         import torch
         if out is None:
             out = torch.zeros(self.n_tets, dtype=torch.float32,
                               device=proj.device if isinstance(proj, torch.Tensor) else "cpu")
-        st = tet_backproject(self.handle, geom, proj, out, accumulate, stats=stats)
+        st = tet_backproject(self.handle, geom, proj, out, accumulate, stats=stats, opts=opts)
         return (out, st) if stats else out

@@ -172,3 +172,25 @@ def test_full_size_c3_sampled():
     rowsum = tm.project(w.geom, ones_t).double().sum().item()
     colsum = tm.backproject(w.geom, ones_r).double().sum().item()
     assert abs(rowsum - colsum) / rowsum <= U.ADJ_TOL
+
+
+def test_paper_mt_modes_run_and_agree_on_generic_rays():
+    """NEXT-1: the paper's Alg. 1/2 walker (fp64) agrees with the exact walker
+    on generic rays of the ball mesh; fp32 runs and reports its failures."""
+    import torch
+
+    from paper_1908_06909_b200 import tetproj as T
+    w = CF.workload("c2", n_angles=2, n_u=64, n_v=48)
+    tm = T.TetMesh.from_mesh(w.mesh)
+    mu = torch.from_numpy(w.mu).cuda()
+    ref, st0 = tm.project(w.geom, mu, stats=True)
+    p64, st64 = tm.project(w.geom, mu, stats=True, opts=T.options(T.TET_TRAVERSE_MT_F64))
+    p32, st32 = tm.project(w.geom, mu, stats=True, opts=T.options(T.TET_TRAVERSE_MT_F32))
+    assert st0["lost"] == 0 and st0["escalations"] == 0
+    ref, p64 = ref.cpu().numpy(), p64.cpu().numpy()
+    err = U.fwd_errors(p64.astype(np.float64), ref.astype(np.float64), w.mu, w.mesh)
+    assert (err <= 1e-4).mean() >= 0.999, (err > 1e-4).sum()
+    assert st64["rays_hit"] == st0["rays_hit"] and st32["rays_hit"] == st0["rays_hit"]
+    x, stb = tm.backproject(w.geom, torch.from_numpy(w.y).cuda(), stats=True,
+                            opts=T.options(T.TET_TRAVERSE_MT_F64))
+    assert stb["crossings"] > 0
