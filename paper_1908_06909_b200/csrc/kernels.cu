@@ -597,7 +597,9 @@ cudaError_t launch_mt(const DevMesh& m, const LaunchChunk& c, bool back, bool si
                       const MtOptions& o, const int* entry, const float* mu_int, float* proj,
                       const float* y, double* acc, unsigned long long* stats, cudaStream_t s) {
     const dim3 grid(((c.nu + 15) / 16) * ((c.nv + 7) / 8), c.n_angles);
-    const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
+    // loop detection for the MT modes: 10 ceil(T^(1/3)) + 100 elements per ray
+    // (SPEC.md:315 reading) -- a straight line crosses O(T^(1/3)) elements
+    const int steps = 10 * (int)ceil(cbrt((double)m.nt)) + 100;
 #define MT_ARGS m.rec, m.tnode, m.vtx, c.ang, c.beam, c.nv, c.nu, m.g, m.C[0], m.C[1], m.C[2], \
                 steps, o.eps0, o.eps_growth, o.max_escalations, entry, mu_int, proj, y, acc, stats
     if (single) {
