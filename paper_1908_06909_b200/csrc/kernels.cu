@@ -271,16 +271,66 @@ __global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ tno
     }
     if (u0 > u1 || v0 > v1) return;
     const int bw = u1 - u0 + 1;
-    const long long npx = (long long)bw * (v1 - v0 + 1);
+    const int npx = bw * (v1 - v0 + 1);
     const int code = (hk.x << 2) | k;
+    // Each edge side is affine in the pixel indices: side(u,v) = c + u*al + v*be
+    // with exact integer coefficients (computed once per block in int128):
+    //   cone:     side = (P00 - S + uU + vV) . ((a-S) x (b-S))
+    //   parallel: side = d . ((a+d) x (b+d)) + (P00 + uU + vV) . (d x (b-a))
+    // Rounded to double, the value at any pixel of the box is within
+    // 4 eps (|c| + u1 |al| + v1 |be|) of the exact side (conversion + 2 FMAs).
+    __shared__ double s_c[3], s_al[3], s_be[3], s_bnd[3];
+    if (threadIdx.x < 3) {
+        const int4 E0 = threadIdx.x == 0 ? A : (threadIdx.x == 1 ? B : C);
+        const int4 E1 = threadIdx.x == 0 ? B : (threadIdx.x == 1 ? C : A);
+        i128 c, al, be;
+        if (beam == TET_BEAM_CONE) {
+            const i128 ax = (i128)E0.x - G.o[0], ay = (i128)E0.y - G.o[1], az = (i128)E0.z - G.o[2];
+            const i128 bx = (i128)E1.x - G.o[0], by = (i128)E1.y - G.o[1], bz = (i128)E1.z - G.o[2];
+            const i128 nx = ay * bz - az * by, ny = az * bx - ax * bz, nz = ax * by - ay * bx;
+            c = (i128)(G.p00[0] - G.o[0]) * nx + (i128)(G.p00[1] - G.o[1]) * ny +
+                (i128)(G.p00[2] - G.o[2]) * nz;
+            al = (i128)G.du[0] * nx + (i128)G.du[1] * ny + (i128)G.du[2] * nz;
+            be = (i128)G.dv[0] * nx + (i128)G.dv[1] * ny + (i128)G.dv[2] * nz;
+        } else {
+            const long long dx = G.o[0], dy = G.o[1], dz = G.o[2];
+            const i128 ax = (i128)E0.x + dx, ay = (i128)E0.y + dy, az = (i128)E0.z + dz;
+            const i128 bx = (i128)E1.x + dx, by = (i128)E1.y + dy, bz = (i128)E1.z + dz;
+            const i128 ex = (i128)E1.x - E0.x, ey = (i128)E1.y - E0.y, ez = (i128)E1.z - E0.z;
+            const i128 mx = dy * ez - dz * ey, my = dz * ex - dx * ez, mz = dx * ey - dy * ex;
+            c = dx * (ay * bz - az * by) + dy * (az * bx - ax * bz) + dz * (ax * by - ay * bx) +
+                (i128)G.p00[0] * mx + (i128)G.p00[1] * my + (i128)G.p00[2] * mz;
+            al = (i128)G.du[0] * mx + (i128)G.du[1] * my + (i128)G.du[2] * mz;
+            be = (i128)G.dv[0] * mx + (i128)G.dv[1] * my + (i128)G.dv[2] * mz;
+        }
+        const double cd = (double)c, ad = (double)al, bd = (double)be;
+        s_c[threadIdx.x] = cd;
+        s_al[threadIdx.x] = ad;
+        s_be[threadIdx.x] = bd;
+        s_bnd[threadIdx.x] = 0x1p-50 * (fabs(cd) + (double)u1 * fabs(ad) + (double)v1 * fabs(bd));
+    }
+    __syncthreads();
+    const double c0 = s_c[0], al0 = s_al[0], be0 = s_be[0], b0 = s_bnd[0];
+    const double c1 = s_c[1], al1 = s_al[1], be1 = s_be[1], b1 = s_bnd[1];
+    const double c2 = s_c[2], al2 = s_al[2], be2 = s_be[2], b2 = s_bnd[2];
     unsigned conflicts = 0, exact = 0;
-    for (long long i = threadIdx.x; i < npx; i += blockDim.x) {
-        const int u = u0 + (int)(i % bw), v = v0 + (int)(i / bw);
-        const RayPts r = ray_points(G, beam, u, v);
+    for (int i = threadIdx.x; i < npx; i += blockDim.x) {
+        const int dv = i / bw;
+        const int u = u0 + (i - dv * bw), v = v0 + dv;
+        const double fu = (double)u, fv = (double)v;
         // entering iff side(a,b) = side(b,c) = side(c,a) = -1 (outward order)
-        if (side_direct(A, B, r, exact) != -1) continue;
-        if (side_direct(B, C, r, exact) != -1) continue;
-        if (side_direct(C, A, r, exact) != -1) continue;
+        const double sab = fma(fv, be0, fma(fu, al0, c0));
+        if (sab > b0) continue;
+        const double sbc = fma(fv, be1, fma(fu, al1, c1));
+        if (sbc > b1) continue;
+        const double sca = fma(fv, be2, fma(fu, al2, c2));
+        if (sca > b2) continue;
+        if (sab >= -b0 || sbc >= -b1 || sca >= -b2) {   // a sign the bound cannot certify
+            const RayPts r = ray_points(G, beam, u, v);
+            if (side_direct(A, B, r, exact) != -1) continue;
+            if (side_direct(B, C, r, exact) != -1) continue;
+            if (side_direct(C, A, r, exact) != -1) continue;
+        }
         const int old = atomicExch(entry + ((size_t)a * nv + v) * nu + u, code);
         conflicts += (old != -1);
     }
