@@ -222,13 +222,15 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(g->n_angles, (1LL << 26) / per_angle));
         int* entry;
         CU(sc.alloc((void**)&entry, sizeof(int) * per_angle * chunk));
+        void* entry_scratch;
+        CU(sc.alloc(&entry_scratch, entry_scratch_bytes(m->dev, chunk)));
         for (int a0 = 0; a0 < g->n_angles; a0 += chunk) {
             const int na = std::min(chunk, g->n_angles - a0);
             LaunchChunk c{d_ang + a0, d_aux + a0, g->beam, na, g->n_v, g->n_u};
             CU(cudaMemsetAsync(entry, 0xff, sizeof(int) * per_angle * na, s));
             {
                 KernelTimer kt(m, TET_K_ENTRY, s);
-                CU(launch_entry(m->dev, c, entry, d_stats, s));
+                CU(launch_entry(m->dev, c, entry, entry_scratch, d_stats, s));
             }
             const size_t off = (size_t)a0 * per_angle;
             const bool fwd = op == Op::Forward;

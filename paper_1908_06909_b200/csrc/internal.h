@@ -84,7 +84,8 @@ struct LaunchChunk {
 };
 
 // kernel launchers (kernels.cu)
-cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry,
+size_t entry_scratch_bytes(const DevMesh& m, int n_angles);
+cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry, void* scratch,
                          unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
                            const float* mu_int, float* proj, unsigned long long* stats,

@@ -199,29 +199,43 @@ __device__ __forceinline__ int side_direct(const int4 a, const int4 b, const Ray
     return sos_side(a.x, a.y, a.z, b.x, b.y, b.z, r.ox, r.oy, r.oz, r.px, r.py, r.pz);
 }
 
-__global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ tnode,
-                                                    const int4* __restrict__ vtx,
-                                                    const int2* __restrict__ hull,
-                                                    const AngleGeom* __restrict__ ang,
-                                                    const AngleAux* __restrict__ aux, int beam,
-                                                    int nv, int nu, int* __restrict__ entry,
-                                                    unsigned long long* __restrict__ stats) {
-    const int h = blockIdx.x, a = blockIdx.y;
+// Work item of the entry finder: one non-culled (hull face, angle) pair.
+struct EntryItem {
+    double c[3], al[3], be[3], bnd[3];  // side_e(u,v) = c + u al + v be, |error| <= bnd
+    int ia, ib, ic;                     // face vertices (outward order)
+    int a, u0, v0, bw, npx, code;       // angle, footprint box, tet<<2|k
+    int pad[3];
+};
+
+// Kernel 1 (one thread per (hull face, angle)): cull the faces that every
+// detector-corner ray leaves through, bound the face's detector footprint,
+// and compute each edge side as an exact affine function of the pixel
+// indices (int128, once per item):
+//   cone:     side(u,v) = (P00 - S + uU + vV) . ((a-S) x (b-S))
+//   parallel: side(u,v) = d . ((a+d) x (b+d)) + (P00 + uU + vV) . (d x (b-a))
+// Rounded to double, side at any pixel of the box is within
+// 4 eps (|c| + u1|al| + v1|be|) of the exact value (conversion + 2 FMAs).
+__global__ void __launch_bounds__(128) entry_setup_kernel(
+    const int4* __restrict__ tnode, const int4* __restrict__ vtx, const int2* __restrict__ hull,
+    int nb, const AngleGeom* __restrict__ ang, const AngleAux* __restrict__ aux, int beam,
+    int n_angles, int nv, int nu, EntryItem* __restrict__ items, unsigned* __restrict__ count) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nb * n_angles) return;
+    const int h = idx % nb, a = idx / nb;
     const int2 hk = hull[h];
     const int4 nodes = __ldg(tnode + hk.x);
     const int k = hk.y;
-    // outward order of face k (opposite node k)
-    int ia, ib, ic;
+    int ia, ib, ic;   // outward order of face k (opposite node k)
     if (k == 0)      { ia = nodes.y; ib = nodes.z; ic = nodes.w; }
     else if (k == 1) { ia = nodes.x; ib = nodes.w; ic = nodes.z; }
     else if (k == 2) { ia = nodes.x; ib = nodes.y; ic = nodes.w; }
     else             { ia = nodes.x; ib = nodes.z; ic = nodes.y; }
-    const int4 A = __ldg(vtx + ia), B = __ldg(vtx + ib), C = __ldg(vtx + ic);
+    const int4 V[3] = {__ldg(vtx + ia), __ldg(vtx + ib), __ldg(vtx + ic)};
     const AngleGeom G = ang[a];
     const AngleAux X = aux[a];
     // --- cull: every detector-corner ray leaves through this face's plane
-    const double e1[3] = {(double)B.x - A.x, (double)B.y - A.y, (double)B.z - A.z};
-    const double e2[3] = {(double)C.x - A.x, (double)C.y - A.y, (double)C.z - A.z};
+    const double e1[3] = {(double)V[1].x - V[0].x, (double)V[1].y - V[0].y, (double)V[1].z - V[0].z};
+    const double e2[3] = {(double)V[2].x - V[0].x, (double)V[2].y - V[0].y, (double)V[2].z - V[0].z};
     const double n[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
                          e1[0] * e2[1] - e1[1] * e2[0]};
     const double nn = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
@@ -237,9 +251,8 @@ __global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ tno
     // --- detector footprint (bounding box, 1 px margin)
     double umin = 1e300, umax = -1e300, vmin = 1e300, vmax = -1e300;
     bool full = false;
-    const int4 V3[3] = {A, B, C};
     for (int j = 0; j < 3; ++j) {
-        const double P[3] = {(double)V3[j].x, (double)V3[j].y, (double)V3[j].z};
+        const double P[3] = {(double)V[j].x, (double)V[j].y, (double)V[j].z};
         double Q[3];
         if (beam == TET_BEAM_CONE) {
             const double dX[3] = {P[0] - X.S[0], P[1] - X.S[1], P[2] - X.S[2]};
@@ -251,9 +264,9 @@ __global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ tno
             for (int i = 0; i < 3; ++i) Q[i] = X.S[i] + lam * dX[i];
         } else {
             const double dN = X.S[0] * X.N[0] + X.S[1] * X.N[1] + X.S[2] * X.N[2];
-            const double s = ((P[0] - X.P00[0]) * X.N[0] + (P[1] - X.P00[1]) * X.N[1] +
-                              (P[2] - X.P00[2]) * X.N[2]) / dN;
-            for (int i = 0; i < 3; ++i) Q[i] = P[i] - s * X.S[i];
+            const double sc = ((P[0] - X.P00[0]) * X.N[0] + (P[1] - X.P00[1]) * X.N[1] +
+                               (P[2] - X.P00[2]) * X.N[2]) / dN;
+            for (int i = 0; i < 3; ++i) Q[i] = P[i] - sc * X.S[i];
         }
         const double w[3] = {Q[0] - X.P00[0], Q[1] - X.P00[1], Q[2] - X.P00[2]};
         const double uu = w[0] * X.Us[0] + w[1] * X.Us[1] + w[2] * X.Us[2];
@@ -270,19 +283,9 @@ __global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ tno
         v1 = (int)fmin((double)(nv - 1), ceil(vmax) + 1.0);
     }
     if (u0 > u1 || v0 > v1) return;
-    const int bw = u1 - u0 + 1;
-    const int npx = bw * (v1 - v0 + 1);
-    const int code = (hk.x << 2) | k;
-    // Each edge side is affine in the pixel indices: side(u,v) = c + u*al + v*be
-    // with exact integer coefficients (computed once per block in int128):
-    //   cone:     side = (P00 - S + uU + vV) . ((a-S) x (b-S))
-    //   parallel: side = d . ((a+d) x (b+d)) + (P00 + uU + vV) . (d x (b-a))
-    // Rounded to double, the value at any pixel of the box is within
-    // 4 eps (|c| + u1 |al| + v1 |be|) of the exact side (conversion + 2 FMAs).
-    __shared__ double s_c[3], s_al[3], s_be[3], s_bnd[3];
-    if (threadIdx.x < 3) {
-        const int4 E0 = threadIdx.x == 0 ? A : (threadIdx.x == 1 ? B : C);
-        const int4 E1 = threadIdx.x == 0 ? B : (threadIdx.x == 1 ? C : A);
+    EntryItem it;
+    for (int e = 0; e < 3; ++e) {
+        const int4 E0 = V[e], E1 = V[e == 2 ? 0 : e + 1];
         i128 c, al, be;
         if (beam == TET_BEAM_CONE) {
             const i128 ax = (i128)E0.x - G.o[0], ay = (i128)E0.y - G.o[1], az = (i128)E0.z - G.o[2];
@@ -303,36 +306,67 @@ __global__ void __launch_bounds__(256) entry_kernel(const int4* __restrict__ tno
             al = (i128)G.du[0] * mx + (i128)G.du[1] * my + (i128)G.du[2] * mz;
             be = (i128)G.dv[0] * mx + (i128)G.dv[1] * my + (i128)G.dv[2] * mz;
         }
-        const double cd = (double)c, ad = (double)al, bd = (double)be;
-        s_c[threadIdx.x] = cd;
-        s_al[threadIdx.x] = ad;
-        s_be[threadIdx.x] = bd;
-        s_bnd[threadIdx.x] = 0x1p-50 * (fabs(cd) + (double)u1 * fabs(ad) + (double)v1 * fabs(bd));
+        it.c[e] = (double)c;
+        it.al[e] = (double)al;
+        it.be[e] = (double)be;
+        it.bnd[e] = 0x1p-50 * (fabs(it.c[e]) + (double)u1 * fabs(it.al[e]) + (double)v1 * fabs(it.be[e]));
     }
-    __syncthreads();
-    const double c0 = s_c[0], al0 = s_al[0], be0 = s_be[0], b0 = s_bnd[0];
-    const double c1 = s_c[1], al1 = s_al[1], be1 = s_be[1], b1 = s_bnd[1];
-    const double c2 = s_c[2], al2 = s_al[2], be2 = s_be[2], b2 = s_bnd[2];
+    it.ia = ia; it.ib = ib; it.ic = ic;
+    it.a = a; it.u0 = u0; it.v0 = v0; it.bw = u1 - u0 + 1;
+    it.npx = (u1 - u0 + 1) * (v1 - v0 + 1);
+    it.code = (hk.x << 2) | k;
+    it.pad[0] = it.pad[1] = it.pad[2] = 0;
+    items[atomicAdd(count, 1u)] = it;
+}
+
+// Rare path of the entry test: all three signs decided by side_direct (fp64
+// static filter, else int128 + SoS).
+__device__ __noinline__ bool exact_entering(const int4* __restrict__ vtx,
+                                            const AngleGeom* __restrict__ ang, int beam, int a,
+                                            int u, int v, int ia, int ib, int ic,
+                                            unsigned& exact) {
+    const RayPts r = ray_points(ang[a], beam, u, v);
+    const int4 A = __ldg(vtx + ia), B = __ldg(vtx + ib), C = __ldg(vtx + ic);
+    return side_direct(A, B, r, exact) == -1 && side_direct(B, C, r, exact) == -1 &&
+           side_direct(C, A, r, exact) == -1;
+}
+
+// Kernel 2 (one warp per work item, grid-stride): the exact entering test for
+// every pixel of the item's box -- entering iff side(a,b) = side(b,c) =
+// side(c,a) = -1 for the outward-ordered face; the affine value certifies a
+// sign when it clears the item's bound, otherwise the int128 + SoS path
+// decides.  Writes entry[ray] = tet<<2 | k and counts conflicts (must be 0).
+__global__ void __launch_bounds__(256) entry_raster_kernel(
+    const int4* __restrict__ vtx, const AngleGeom* __restrict__ ang, int beam, int nv, int nu,
+    const EntryItem* __restrict__ items, const unsigned* __restrict__ count,
+    int* __restrict__ entry, unsigned long long* __restrict__ stats) {
+    const unsigned n_items = *count;
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int n_warps = (gridDim.x * blockDim.x) >> 5;
     unsigned conflicts = 0, exact = 0;
-    for (int i = threadIdx.x; i < npx; i += blockDim.x) {
-        const int dv = i / bw;
-        const int u = u0 + (i - dv * bw), v = v0 + dv;
-        const double fu = (double)u, fv = (double)v;
-        // entering iff side(a,b) = side(b,c) = side(c,a) = -1 (outward order)
-        const double sab = fma(fv, be0, fma(fu, al0, c0));
-        if (sab > b0) continue;
-        const double sbc = fma(fv, be1, fma(fu, al1, c1));
-        if (sbc > b1) continue;
-        const double sca = fma(fv, be2, fma(fu, al2, c2));
-        if (sca > b2) continue;
-        if (sab >= -b0 || sbc >= -b1 || sca >= -b2) {   // a sign the bound cannot certify
-            const RayPts r = ray_points(G, beam, u, v);
-            if (side_direct(A, B, r, exact) != -1) continue;
-            if (side_direct(B, C, r, exact) != -1) continue;
-            if (side_direct(C, A, r, exact) != -1) continue;
+    for (unsigned w = warp; w < n_items; w += n_warps) {
+        const EntryItem& it = items[w];
+        const double c0 = it.c[0], al0 = it.al[0], be0 = it.be[0], b0 = it.bnd[0];
+        const double c1 = it.c[1], al1 = it.al[1], be1 = it.be[1], b1 = it.bnd[1];
+        const double c2 = it.c[2], al2 = it.al[2], be2 = it.be[2], b2 = it.bnd[2];
+        const int bw = it.bw, npx = it.npx, u0 = it.u0, v0 = it.v0, a = it.a, code = it.code;
+        for (int i = lane; i < npx; i += 32) {
+            const int dv = i / bw;
+            const int u = u0 + (i - dv * bw), v = v0 + dv;
+            const double fu = (double)u, fv = (double)v;
+            const double sab = fma(fv, be0, fma(fu, al0, c0));
+            if (sab > b0) continue;
+            const double sbc = fma(fv, be1, fma(fu, al1, c1));
+            if (sbc > b1) continue;
+            const double sca = fma(fv, be2, fma(fu, al2, c2));
+            if (sca > b2) continue;
+            if (sab >= -b0 || sbc >= -b1 || sca >= -b2) {   // a sign the bound cannot certify
+                if (!exact_entering(vtx, ang, beam, a, u, v, it.ia, it.ib, it.ic, exact)) continue;
+            }
+            const int old = atomicExch(entry + ((size_t)a * nv + v) * nu + u, code);
+            conflicts += (old != -1);
         }
-        const int old = atomicExch(entry + ((size_t)a * nv + v) * nu + u, code);
-        conflicts += (old != -1);
     }
     if (conflicts) atomicAdd(stats + ST_CONFLICT, (unsigned long long)conflicts);
     if (exact) atomicAdd(stats + ST_EXACT, (unsigned long long)exact);
@@ -693,11 +727,21 @@ static int grid_for(int64_t n) {
 }
 
 // ----------------------------------------------------------- launchers --
-cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry,
+size_t entry_scratch_bytes(const DevMesh& m, int n_angles) {
+    return sizeof(EntryItem) * (size_t)m.nb * n_angles + 256;
+}
+
+cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry, void* scratch,
                          unsigned long long* stats, cudaStream_t s) {
-    dim3 grid((unsigned)m.nb, (unsigned)c.n_angles);
-    entry_kernel<<<grid, 256, 0, s>>>(m.tnode, m.vtx, m.hull, c.ang, c.aux, c.beam, c.nv, c.nu,
-                                      entry, stats);
+    unsigned* count = (unsigned*)scratch;
+    EntryItem* items = (EntryItem*)((char*)scratch + 256);
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    const long long n = (long long)m.nb * c.n_angles;
+    entry_setup_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
+        m.tnode, m.vtx, m.hull, (int)m.nb, c.ang, c.aux, c.beam, c.n_angles, c.nv, c.nu, items, count);
+    entry_raster_kernel<<<148 * 8, 256, 0, s>>>(m.vtx, c.ang, c.beam, c.nv, c.nu, items, count,
+                                                entry, stats);
     return cudaGetLastError();
 }
 
