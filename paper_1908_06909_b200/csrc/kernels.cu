@@ -218,7 +218,7 @@ struct EntryItem {
 __global__ void __launch_bounds__(128) entry_setup_kernel(
     const int4* __restrict__ tnode, const int4* __restrict__ vtx, const int2* __restrict__ hull,
     int nb, const AngleGeom* __restrict__ ang, const AngleAux* __restrict__ aux, int beam,
-    int n_angles, int nv, int nu, EntryItem* __restrict__ items, unsigned* __restrict__ count) {
+    int n_angles, int nv, int nu, EntryItem* __restrict__ items) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= nb * n_angles) return;
     const int h = idx % nb, a = idx / nb;
@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(128) entry_setup_kernel(
         const double dd = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
         cull = dn > 1e-9 * dd * nn;
     }
+    items[idx].npx = 0;   // dense item array: culled / empty items stay empty
     if (cull) return;
     // --- detector footprint (bounding box, 1 px margin)
     double umin = 1e300, umax = -1e300, vmin = 1e300, vmax = -1e300;
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(128) entry_setup_kernel(
     it.npx = (u1 - u0 + 1) * (v1 - v0 + 1);
     it.code = (hk.x << 2) | k;
     it.pad[0] = it.pad[1] = it.pad[2] = 0;
-    items[atomicAdd(count, 1u)] = it;
+    items[idx] = it;
 }
 
 // Rare path of the entry test: all three signs decided by side_direct (fp64
@@ -331,42 +332,39 @@ __device__ __noinline__ bool exact_entering(const int4* __restrict__ vtx,
            side_direct(C, A, r, exact) == -1;
 }
 
-// Kernel 2 (one warp per work item, grid-stride): the exact entering test for
+// Kernel 2 (one block per (face, angle) item; empty items exit at once, the
+// block scheduler balances the uneven footprints): the exact entering test for
 // every pixel of the item's box -- entering iff side(a,b) = side(b,c) =
 // side(c,a) = -1 for the outward-ordered face; the affine value certifies a
 // sign when it clears the item's bound, otherwise the int128 + SoS path
 // decides.  Writes entry[ray] = tet<<2 | k and counts conflicts (must be 0).
-__global__ void __launch_bounds__(256) entry_raster_kernel(
+__global__ void __launch_bounds__(128, 8) entry_raster_kernel(
     const int4* __restrict__ vtx, const AngleGeom* __restrict__ ang, int beam, int nv, int nu,
-    const EntryItem* __restrict__ items, const unsigned* __restrict__ count,
-    int* __restrict__ entry, unsigned long long* __restrict__ stats) {
-    const unsigned n_items = *count;
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int n_warps = (gridDim.x * blockDim.x) >> 5;
+    const EntryItem* __restrict__ items, int* __restrict__ entry,
+    unsigned long long* __restrict__ stats) {
+    const EntryItem* it = items + blockIdx.x;
+    const int npx = it->npx;
+    if (npx == 0) return;
     unsigned conflicts = 0, exact = 0;
-    for (unsigned w = warp; w < n_items; w += n_warps) {
-        const EntryItem& it = items[w];
-        const double c0 = it.c[0], al0 = it.al[0], be0 = it.be[0], b0 = it.bnd[0];
-        const double c1 = it.c[1], al1 = it.al[1], be1 = it.be[1], b1 = it.bnd[1];
-        const double c2 = it.c[2], al2 = it.al[2], be2 = it.be[2], b2 = it.bnd[2];
-        const int bw = it.bw, npx = it.npx, u0 = it.u0, v0 = it.v0, a = it.a, code = it.code;
-        for (int i = lane; i < npx; i += 32) {
-            const int dv = i / bw;
-            const int u = u0 + (i - dv * bw), v = v0 + dv;
-            const double fu = (double)u, fv = (double)v;
-            const double sab = fma(fv, be0, fma(fu, al0, c0));
-            if (sab > b0) continue;
-            const double sbc = fma(fv, be1, fma(fu, al1, c1));
-            if (sbc > b1) continue;
-            const double sca = fma(fv, be2, fma(fu, al2, c2));
-            if (sca > b2) continue;
-            if (sab >= -b0 || sbc >= -b1 || sca >= -b2) {   // a sign the bound cannot certify
-                if (!exact_entering(vtx, ang, beam, a, u, v, it.ia, it.ib, it.ic, exact)) continue;
-            }
-            const int old = atomicExch(entry + ((size_t)a * nv + v) * nu + u, code);
-            conflicts += (old != -1);
+    const double c0 = it->c[0], al0 = it->al[0], be0 = it->be[0], b0 = it->bnd[0];
+    const double c1 = it->c[1], al1 = it->al[1], be1 = it->be[1], b1 = it->bnd[1];
+    const double c2 = it->c[2], al2 = it->al[2], be2 = it->be[2], b2 = it->bnd[2];
+    const int bw = it->bw, u0 = it->u0, v0 = it->v0, a = it->a, code = it->code;
+    for (int i = threadIdx.x; i < npx; i += blockDim.x) {
+        const int dv = i / bw;
+        const int u = u0 + (i - dv * bw), v = v0 + dv;
+        const double fu = (double)u, fv = (double)v;
+        const double sab = fma(fv, be0, fma(fu, al0, c0));
+        if (sab > b0) continue;
+        const double sbc = fma(fv, be1, fma(fu, al1, c1));
+        if (sbc > b1) continue;
+        const double sca = fma(fv, be2, fma(fu, al2, c2));
+        if (sca > b2) continue;
+        if (sab >= -b0 || sbc >= -b1 || sca >= -b2) {   // a sign the bound cannot certify
+            if (!exact_entering(vtx, ang, beam, a, u, v, it->ia, it->ib, it->ic, exact)) continue;
         }
+        const int old = atomicExch(entry + ((size_t)a * nv + v) * nu + u, code);
+        conflicts += (old != -1);
     }
     if (conflicts) atomicAdd(stats + ST_CONFLICT, (unsigned long long)conflicts);
     if (exact) atomicAdd(stats + ST_EXACT, (unsigned long long)exact);
@@ -733,15 +731,12 @@ size_t entry_scratch_bytes(const DevMesh& m, int n_angles) {
 
 cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry, void* scratch,
                          unsigned long long* stats, cudaStream_t s) {
-    unsigned* count = (unsigned*)scratch;
     EntryItem* items = (EntryItem*)((char*)scratch + 256);
-    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned), s);
-    if (e != cudaSuccess) return e;
     const long long n = (long long)m.nb * c.n_angles;
     entry_setup_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
-        m.tnode, m.vtx, m.hull, (int)m.nb, c.ang, c.aux, c.beam, c.n_angles, c.nv, c.nu, items, count);
-    entry_raster_kernel<<<148 * 8, 256, 0, s>>>(m.vtx, c.ang, c.beam, c.nv, c.nu, items, count,
-                                                entry, stats);
+        m.tnode, m.vtx, m.hull, (int)m.nb, c.ang, c.aux, c.beam, c.n_angles, c.nv, c.nu, items);
+    entry_raster_kernel<<<(unsigned)n, 128, 0, s>>>(m.vtx, c.ang, c.beam, c.nv, c.nu, items, entry,
+                                                    stats);
     return cudaGetLastError();
 }
 
