@@ -209,9 +209,9 @@ def main():
     from paper_1908_06909_b200.dist import dist_backproject
 
     ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1 and rank != 0:
         dist.barrier()                      # rank 0 builds the mesh cache first

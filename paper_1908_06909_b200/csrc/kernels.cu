@@ -154,6 +154,70 @@ __device__ __forceinline__ void xform(const Frame& F, const int4 v, double& x, d
     y = fma(-F.sy, z, a2);
 }
 
+// Compile-time axis variants of the shear frame: AX = 2*k + swap (k = shear
+// axis, swap = D_k < 0) for AX < 6; AX = 6 is the generic per-ray frame.  A
+// block uses a fixed variant when its tile's rays are all dominated by the
+// same axis with the same sign (trace_kernel), which removes the per-vertex
+// component selects and the permutation registers.
+template <int AX>
+struct Axis {
+    static constexpr int k = AX >> 1;
+    static constexpr int c1 = k == 0 ? 1 : (k == 1 ? 2 : 0);
+    static constexpr int c2 = k == 0 ? 2 : (k == 1 ? 0 : 1);
+    static constexpr int K1 = (AX & 1) ? c2 : c1;
+    static constexpr int K2 = (AX & 1) ? c1 : c2;
+};
+
+template <int C>
+__device__ __forceinline__ long long pick(long long x, long long y, long long z) {
+    return C == 0 ? x : (C == 1 ? y : z);
+}
+
+template <int C>
+__device__ __forceinline__ int pick4(const int4 v) {
+    return C == 0 ? v.x : (C == 1 ? v.y : v.z);
+}
+
+// Frame with a FIXED axis (k, K1, K2); tau carries the (1 + |sx| + |sy|)^2
+// growth of the shear coordinates when k is not the ray's dominant axis.
+template <int AX>
+__device__ __forceinline__ void make_frame_ax(const RayPts& r, double rmax, double g, Frame& F) {
+    if constexpr (AX == 6) {
+        make_frame(r, rmax, g, F);
+    } else {
+        using A = Axis<AX>;
+        const long long Dx = r.px - r.ox, Dy = r.py - r.oy, Dz = r.pz - r.oz;
+        const double dk = (double)pick<A::k>(Dx, Dy, Dz);
+        F.sx = (double)pick<A::K1>(Dx, Dy, Dz) / dk;
+        F.sy = (double)pick<A::K2>(Dx, Dy, Dz) / dk;
+        F.o1 = (double)pick<A::K1>(r.ox, r.oy, r.oz);
+        F.o2 = (double)pick<A::K2>(r.ox, r.oy, r.oz);
+        F.o3 = (double)pick<A::k>(r.ox, r.oy, r.oz);
+        const double ox = (double)r.ox, oy = (double)r.oy, oz = (double)r.oz;
+        const double amax = (sqrt(ox * ox + oy * oy + oz * oz) + rmax) *
+                            (1.0 + fabs(F.sx) + fabs(F.sy)) * 0.5;
+        F.tau = amax * amax * 0x1p-38;
+        const double dx = (double)Dx, dy = (double)Dy, dz = (double)Dz;
+        F.scale = sqrt(dx * dx + dy * dy + dz * dz) / dk * g;
+        F.k1 = A::K1; F.k2 = A::K2; F.k3 = A::k;
+    }
+}
+
+template <int AX>
+__device__ __forceinline__ void xform_ax(const Frame& F, const int4 v, double& x, double& y,
+                                         double& z) {
+    if constexpr (AX == 6) {
+        xform(F, v, x, y, z);
+    } else {
+        using A = Axis<AX>;
+        const double a1 = (double)pick4<A::K1>(v) - F.o1;   // exact (|.| < 2^33)
+        const double a2 = (double)pick4<A::K2>(v) - F.o2;
+        z = (double)pick4<A::k>(v) - F.o3;
+        x = fma(-F.sx, z, a1);
+        y = fma(-F.sy, z, a2);
+    }
+}
+
 __device__ __forceinline__ double side2(double xa, double ya, double xb, double yb) {
     return fma(xa, yb, -(ya * xb));
 }
@@ -386,35 +450,18 @@ __global__ void __launch_bounds__(128, 8) entry_raster_kernel(
 // the apex vertex are gathered IN PARALLEL (the tag carried the apex id);
 // the tag of the exit face gives the next tet, its apex and the local-index
 // map, so the neighbour's node list is never loaded.
-template <bool BACK, int MINB>
-__global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict__ rec,
-                                                          const int4* __restrict__ tnode,
-                                                          const int4* __restrict__ vtx,
-                                                          const AngleGeom* __restrict__ ang,
-                                                          int beam, int nv, int nu, double rmax,
-                                                          double g, int max_steps,
-                                                          const int* __restrict__ entry,
-                                                          const float* __restrict__ mu,
-                                                          float* __restrict__ proj,
-                                                          const float* __restrict__ y,
-                                                          double* __restrict__ acc,
-                                                          unsigned long long* __restrict__ stats) {
-    const int tiles_u = (nu + 15) >> 4;
-    const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
-    const int a = blockIdx.y;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int u = bx * 16 + (w & 1) * 8 + (lane & 7);
-    const int v = by * 8 + (w >> 1) * 4 + (lane >> 3);
-    const bool valid = u < nu && v < nv;
-    const size_t rid = ((size_t)a * nv + v) * nu + u;
-    const int e = valid ? entry[rid] : -1;
-
-    unsigned n_cross = 0, n_exact = 0, n_lost = 0, n_stuck = 0;
-    double sum = 0.0;
-    if (e >= 0) {
+template <bool BACK, int AX>
+__device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int4* __restrict__ tnode,
+                                         const int4* __restrict__ vtx,
+                                         const AngleGeom* __restrict__ ang, int beam, int a, int u,
+                                         int v, double rmax, double g, int max_steps, int e,
+                                         size_t rid, const float* __restrict__ mu,
+                                         const float* __restrict__ y, double* __restrict__ acc,
+                                         double& sum, unsigned& n_cross, unsigned& n_exact,
+                                         unsigned& n_lost, unsigned& n_stuck) {
         const RayPts r = ray_points(ang[a], beam, u, v);
         Frame F;
-        make_frame(r, rmax, g, F);
+        make_frame_ax<AX>(r, rmax, g, F);
         const float yv = BACK ? y[rid] : 0.f;
         int t = e >> 2, kin = e & 3;
         const int4 nodes = __ldg(tnode + t);
@@ -426,9 +473,9 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
         else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; lp = 0 | 2 << 2 | 1 << 4; }
         int iap = sel4(nodes, kin);
         double x0, y0, z0, x1, y1, z1, x2, y2, z2;
-        xform(F, __ldg(vtx + id0), x0, y0, z0);
-        xform(F, __ldg(vtx + id1), x1, y1, z1);
-        xform(F, __ldg(vtx + id2), x2, y2, z2);
+        xform_ax<AX>(F, __ldg(vtx + id0), x0, y0, z0);
+        xform_ax<AX>(F, __ldg(vtx + id1), x1, y1, z1);
+        xform_ax<AX>(F, __ldg(vtx + id2), x2, y2, z2);
         double s01 = side2(x0, y0, x1, y1), s12 = side2(x1, y1, x2, y2), s20 = side2(x2, y2, x0, y0);
         double zin;
         {
@@ -448,7 +495,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
         int4 X = __ldg(vtx + iap);                          // apex vertex (16 B)
         while (true) {
             double x3, y3, z3;
-            xform(F, X, x3, y3, z3);
+            xform_ax<AX>(F, X, x3, y3, z3);
             const double p0 = side2(x3, y3, x0, y0);   // side(apex, slot k)
             const double p1 = side2(x3, y3, x1, y1);
             const double p2 = side2(x3, y3, x2, y2);
@@ -533,6 +580,68 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
             zin = zout;
             iap = (int)(hi >> 8);
         }
+    }
+
+template <bool BACK, int MINB>
+__global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict__ rec,
+                                                          const int4* __restrict__ tnode,
+                                                          const int4* __restrict__ vtx,
+                                                          const AngleGeom* __restrict__ ang,
+                                                          int beam, int nv, int nu, double rmax,
+                                                          double g, int max_steps,
+                                                          const int* __restrict__ entry,
+                                                          const float* __restrict__ mu,
+                                                          float* __restrict__ proj,
+                                                          const float* __restrict__ y,
+                                                          double* __restrict__ acc,
+                                                          unsigned long long* __restrict__ stats) {
+    const int tiles_u = (nu + 15) >> 4;
+    const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
+    const int a = blockIdx.y;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int u = bx * 16 + (w & 1) * 8 + (lane & 7);
+    const int v = by * 8 + (w >> 1) * 4 + (lane >> 3);
+    const bool valid = u < nu && v < nv;
+    const size_t rid = ((size_t)a * nv + v) * nu + u;
+    const int e = valid ? entry[rid] : -1;
+
+    unsigned n_cross = 0, n_exact = 0, n_lost = 0, n_stuck = 0;
+    double sum = 0.0;
+    // Block-uniform shear axis: the tile's centre ray decides; every ray of the
+    // block must be dominated (|D_k| >= max|D|/2) by that axis with the same
+    // sign (block vote), else the generic per-ray frame (variant 6) is used.
+    int ax = 6;
+    {
+        const int uc = min(bx * 16 + 8, nu - 1), vc = min(by * 8 + 4, nv - 1);
+        const RayPts rc = ray_points(ang[a], beam, uc, vc);
+        const long long cx = rc.px - rc.ox, cy = rc.py - rc.oy, cz = rc.pz - rc.oz;
+        const long long ax_ = cx < 0 ? -cx : cx, ay_ = cy < 0 ? -cy : cy, az_ = cz < 0 ? -cz : cz;
+        const int kc = (ax_ >= ay_ && ax_ >= az_) ? 0 : (ay_ >= az_ ? 1 : 2);
+        const long long dkc = kc == 0 ? cx : (kc == 1 ? cy : cz);
+        bool ok = true;
+        if (e >= 0) {
+            const RayPts r = ray_points(ang[a], beam, u, v);
+            const long long dx = r.px - r.ox, dy = r.py - r.oy, dz = r.pz - r.oz;
+            const long long dk = kc == 0 ? dx : (kc == 1 ? dy : dz);
+            const long long adk = dk < 0 ? -dk : dk;
+            const long long m = max(dx < 0 ? -dx : dx, max(dy < 0 ? -dy : dy, dz < 0 ? -dz : dz));
+            ok = (dk < 0) == (dkc < 0) && 2 * adk >= m;
+        }
+        if (__syncthreads_and(ok)) ax = 2 * kc + (dkc < 0 ? 1 : 0);
+    }
+    if (e >= 0) {
+#define WALK(AXV) walk_ray<BACK, AXV>(rec, tnode, vtx, ang, beam, a, u, v, rmax, g, max_steps, e, \
+                                      rid, mu, y, acc, sum, n_cross, n_exact, n_lost, n_stuck)
+        switch (ax) {
+            case 0: WALK(0); break;
+            case 1: WALK(1); break;
+            case 2: WALK(2); break;
+            case 3: WALK(3); break;
+            case 4: WALK(4); break;
+            case 5: WALK(5); break;
+            default: WALK(6); break;
+        }
+#undef WALK
     }
     if (!BACK && valid) proj[rid] = (float)sum;
     add_stat(stats, ST_HIT, e >= 0 ? 1u : 0u);
