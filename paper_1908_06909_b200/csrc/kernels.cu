@@ -563,18 +563,7 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             // crossing may come out as -1e-16 R, which is harmless in the sum
             const double chord = (zout - zin) * F.scale;
             if (BACK) {
-                // warp-aggregated scatter: lanes at the same tet in this step
-                // combine their contributions, the lowest one issues the RED
-                const double val = chord > 0.0 ? chord * (double)yv : 0.0;
-                const unsigned act = __activemask();
-                const unsigned peers = __match_any_sync(act, tcur);
-                double tot = val;
-                if (peers & (peers - 1)) {
-                    tot = 0.0;
-                    for (unsigned m = peers; m; m &= m - 1)
-                        tot += __shfl_sync(peers, val, __ffs(m) - 1);
-                }
-                if ((threadIdx.x & 31) == __ffs(peers) - 1 && tot != 0.0) atomicAdd(acc + tcur, tot);
+                if (chord > 0.0) atomicAdd(acc + tcur, chord * (double)yv);
             } else {
                 sum = fma(chord, (double)mcur, sum);
             }
