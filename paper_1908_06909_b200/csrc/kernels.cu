@@ -594,13 +594,16 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
                                                           float* __restrict__ proj,
                                                           const float* __restrict__ y,
                                                           double* __restrict__ acc,
-                                                          unsigned long long* __restrict__ stats) {
-    const int tiles_u = (nu + 15) >> 4;
+                                                          unsigned long long* __restrict__ stats,
+                                                          int tw_log) {
+    // warp tile: (1 << tw_log) x (32 >> tw_log) pixels; block = 2 x 2 warp tiles
+    const int tw = 1 << tw_log, th = 32 >> tw_log;
+    const int tiles_u = (nu + 2 * tw - 1) / (2 * tw);
     const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
     const int a = blockIdx.y;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int u = bx * 16 + (w & 1) * 8 + (lane & 7);
-    const int v = by * 8 + (w >> 1) * 4 + (lane >> 3);
+    const int u = bx * 2 * tw + (w & 1) * tw + (lane & (tw - 1));
+    const int v = by * 2 * th + (w >> 1) * th + (lane >> tw_log);
     const bool valid = u < nu && v < nv;
     const size_t rid = ((size_t)a * nv + v) * nu + u;
     const int e = valid ? entry[rid] : -1;
@@ -612,7 +615,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
     // sign (block vote), else the generic per-ray frame (variant 6) is used.
     int ax = 6;
     {
-        const int uc = min(bx * 16 + 8, nu - 1), vc = min(by * 8 + 4, nv - 1);
+        const int uc = min(bx * 2 * tw + tw, nu - 1), vc = min(by * 2 * th + th, nv - 1);
         const RayPts rc = ray_points(ang[a], beam, uc, vc);
         const long long cx = rc.px - rc.ox, cy = rc.py - rc.oy, cz = rc.pz - rc.oz;
         const long long ax_ = cx < 0 ? -cx : cx, ay_ = cy < 0 ? -cy : cy, az_ = cz < 0 ? -cz : cz;
@@ -854,6 +857,23 @@ static dim3 trace_grid(const LaunchChunk& c) {
     return dim3(tiles, (unsigned)c.n_angles);
 }
 
+// Warp pixel tile of the exact walker: (1 << tw_log) x (32 >> tw_log); default
+// 8 x 4 (TETPROJ_TILE_W overrides for measurements).
+static int tile_w_log() {
+    static int v = [] {
+        const char* e = getenv("TETPROJ_TILE_W");
+        const int w = e ? atoi(e) : 8;
+        return w == 4 ? 2 : w == 16 ? 4 : w == 32 ? 5 : w == 2 ? 1 : 3;
+    }();
+    return v;
+}
+
+static dim3 trace_grid_w(const LaunchChunk& c, int tw_log) {
+    const int tw = 1 << tw_log, th = 32 >> tw_log;
+    const unsigned tiles = (unsigned)(((c.nu + 2 * tw - 1) / (2 * tw)) * ((c.nv + 2 * th - 1) / (2 * th)));
+    return dim3(tiles, (unsigned)c.n_angles);
+}
+
 #define TRACE_ARGS m.rec, m.tnode, m.vtx, c.ang, c.beam, c.nv, c.nu, m.rmax, m.g, steps, entry, \
                    mu_int, proj, y, acc, stats
 
@@ -865,7 +885,8 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
                          const float* mu_int, float* proj, const float* y, double* acc,
                          unsigned long long* stats, cudaStream_t s) {
     const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
-    trace_kernel<BACK, 4><<<trace_grid(c), 128, 0, s>>>(TRACE_ARGS);
+    const int twl = tile_w_log();
+    trace_kernel<BACK, 4><<<trace_grid_w(c, twl), 128, 0, s>>>(TRACE_ARGS, twl);
 }
 
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
