@@ -21,7 +21,6 @@ struct tet_mesh {
     void* d_rec = nullptr;
     void* d_tnode = nullptr;
     void* d_vtx = nullptr;
-    void* d_vtxd = nullptr;
     void* d_hull = nullptr;
     void* d_perm = nullptr;
     int64_t bytes = 0;
@@ -316,11 +315,6 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     cudaError_t e = up(&m->d_rec, H.rec.data(), H.rec.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_tnode, H.tnode.data(), H.tnode.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_vtx, H.vtx.data(), H.vtx.size() * 4);
-    if (e == cudaSuccess) {
-        std::vector<double> vd(H.vtx.size());
-        for (size_t i = 0; i < vd.size(); ++i) vd[i] = (double)H.vtx[i];
-        e = up(&m->d_vtxd, vd.data(), vd.size() * sizeof(double));
-    }
     if (e == cudaSuccess) e = up(&m->d_hull, H.hull.data(), H.hull.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_perm, H.perm.data(), H.perm.size() * 4);
     if (e != cudaSuccess) {
@@ -330,7 +324,6 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     m->dev.rec = (const int4*)m->d_rec;
     m->dev.tnode = (const int4*)m->d_tnode;
     m->dev.vtx = (const int4*)m->d_vtx;
-    m->dev.vtxd = (const double4*)m->d_vtxd;
     m->dev.hull = (const int2*)m->d_hull;
     m->dev.perm = (const int*)m->d_perm;
     m->dev.nv = H.nv;
@@ -360,7 +353,6 @@ tet_status tet_mesh_destroy(tet_mesh_t m) {
     cudaFree(m->d_rec);
     cudaFree(m->d_tnode);
     cudaFree(m->d_vtx);
-    cudaFree(m->d_vtxd);
     cudaFree(m->d_hull);
     cudaFree(m->d_perm);
     delete m;

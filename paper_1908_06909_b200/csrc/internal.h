@@ -59,8 +59,7 @@ tet_status prepare_geometry(const HostMesh& m, const tet_geometry* g,
 struct DevMesh {
     const int4* rec = nullptr;   // [2T] face tags
     const int4* tnode = nullptr; // [T] node ids
-    const int4* vtx = nullptr;   // [V] grid coordinates (x,y,z,0)
-    const double4* vtxd = nullptr; // [V] the same as doubles (walker fixed-axis variants)
+    const int4* vtx = nullptr;   // [V]
     const int2* hull = nullptr;  // [B]
     const int* perm = nullptr;   // [T]
     int64_t nv = 0, nt = 0, nb = 0;

@@ -17,8 +17,6 @@
 #include <stdint.h>
 #include <stdlib.h>
 
-#include <type_traits>
-
 #include "internal.h"
 
 namespace tetproj {
@@ -203,42 +201,6 @@ __device__ __forceinline__ void make_frame_ax(const RayPts& r, double rmax, doub
         F.scale = sqrt(dx * dx + dy * dy + dz * dz) / dk * g;
         F.k1 = A::K1; F.k2 = A::K2; F.k3 = A::k;
     }
-}
-
-// Vertex record seen by a walker variant: fixed-axis variants read the fp64
-// copy of the grid coordinates (exact integers; one 256-bit load, no I2F on
-// the critical path), the generic variant the int32 coordinates.
-template <int AX>
-using VtxT = typename std::conditional<(AX < 6), double4, int4>::type;
-
-__device__ __forceinline__ double4 ldg_d4(const double4* p) {
-    double4 r;
-    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-        : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
-    return r;
-}
-
-template <int AX>
-__device__ __forceinline__ VtxT<AX> load_vtx(const int4* __restrict__ vtx,
-                                             const double4* __restrict__ vtxd, int id) {
-    if constexpr (AX < 6) return ldg_d4(vtxd + id);
-    else return __ldg(vtx + id);
-}
-
-template <int C>
-__device__ __forceinline__ double pickd(const double4 v) {
-    return C == 0 ? v.x : (C == 1 ? v.y : v.z);
-}
-
-template <int AX>
-__device__ __forceinline__ void xform_ax(const Frame& F, const double4 v, double& x, double& y,
-                                         double& z) {
-    using A = Axis<AX>;
-    const double a1 = pickd<A::K1>(v) - F.o1;   // exact (|.| < 2^33)
-    const double a2 = pickd<A::K2>(v) - F.o2;
-    z = pickd<A::k>(v) - F.o3;
-    x = fma(-F.sx, z, a1);
-    y = fma(-F.sy, z, a2);
 }
 
 template <int AX>
@@ -491,7 +453,6 @@ __global__ void __launch_bounds__(128, 8) entry_raster_kernel(
 template <bool BACK, int AX>
 __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int4* __restrict__ tnode,
                                          const int4* __restrict__ vtx,
-                                         const double4* __restrict__ vtxd,
                                          const AngleGeom* __restrict__ ang, int beam, int a, int u,
                                          int v, double rmax, double g, int max_steps, int e,
                                          size_t rid, const float* __restrict__ mu,
@@ -512,9 +473,9 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
         else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; lp = 0 | 2 << 2 | 1 << 4; }
         int iap = sel4(nodes, kin);
         double x0, y0, z0, x1, y1, z1, x2, y2, z2;
-        xform_ax<AX>(F, load_vtx<AX>(vtx, vtxd, id0), x0, y0, z0);
-        xform_ax<AX>(F, load_vtx<AX>(vtx, vtxd, id1), x1, y1, z1);
-        xform_ax<AX>(F, load_vtx<AX>(vtx, vtxd, id2), x2, y2, z2);
+        xform_ax<AX>(F, __ldg(vtx + id0), x0, y0, z0);
+        xform_ax<AX>(F, __ldg(vtx + id1), x1, y1, z1);
+        xform_ax<AX>(F, __ldg(vtx + id2), x2, y2, z2);
         double s01 = side2(x0, y0, x1, y1), s12 = side2(x1, y1, x2, y2), s20 = side2(x2, y2, x0, y0);
         double zin;
         {
@@ -531,7 +492,7 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
         ldg_rec256(rec + 2 * (size_t)t, ta, tb);             // face tags of t (32 B)
         float mut = 0.f;
         if (!BACK) mut = __ldg(mu + t);
-        VtxT<AX> X = load_vtx<AX>(vtx, vtxd, iap);          // apex vertex
+        int4 X = __ldg(vtx + iap);                          // apex vertex (16 B)
         while (true) {
             double x3, y3, z3;
             xform_ax<AX>(F, X, x3, y3, z3);
@@ -568,7 +529,7 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
                 t = lo >> 2;
                 ldg_rec256(rec + 2 * (size_t)t, ta, tb);
                 if (!BACK) mut = __ldg(mu + t);
-                X = load_vtx<AX>(vtx, vtxd, (int)(hi >> 8));
+                X = __ldg(vtx + (int)(hi >> 8));
                 // local indices in the next tet: kept slots map through `map`,
                 // the dropped slot j receives the current apex (local index kin)
                 const int s0 = selp(kin, lp & 3, d0);
@@ -625,7 +586,6 @@ template <bool BACK, int MINB>
 __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict__ rec,
                                                           const int4* __restrict__ tnode,
                                                           const int4* __restrict__ vtx,
-                                                          const double4* __restrict__ vtxd,
                                                           const AngleGeom* __restrict__ ang,
                                                           int beam, int nv, int nu, double rmax,
                                                           double g, int max_steps,
@@ -673,7 +633,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
         if (__syncthreads_and(ok)) ax = 2 * kc + (dkc < 0 ? 1 : 0);
     }
     if (e >= 0) {
-#define WALK(AXV) walk_ray<BACK, AXV>(rec, tnode, vtx, vtxd, ang, beam, a, u, v, rmax, g, max_steps, e, \
+#define WALK(AXV) walk_ray<BACK, AXV>(rec, tnode, vtx, ang, beam, a, u, v, rmax, g, max_steps, e, \
                                       rid, mu, y, acc, sum, n_cross, n_exact, n_lost, n_stuck)
         switch (ax) {
             case 0: WALK(0); break;
@@ -892,6 +852,11 @@ cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry, voi
     return cudaGetLastError();
 }
 
+static dim3 trace_grid(const LaunchChunk& c) {
+    const unsigned tiles = (unsigned)(((c.nu + 15) / 16) * ((c.nv + 7) / 8));
+    return dim3(tiles, (unsigned)c.n_angles);
+}
+
 // Warp pixel tile of the exact walker: (1 << tw_log) x (32 >> tw_log); default
 // 8 x 4 (TETPROJ_TILE_W overrides for measurements).
 static int tile_w_log() {
@@ -909,7 +874,7 @@ static dim3 trace_grid_w(const LaunchChunk& c, int tw_log) {
     return dim3(tiles, (unsigned)c.n_angles);
 }
 
-#define TRACE_ARGS m.rec, m.tnode, m.vtx, m.vtxd, c.ang, c.beam, c.nv, c.nu, m.rmax, m.g, steps, entry, \
+#define TRACE_ARGS m.rec, m.tnode, m.vtx, c.ang, c.beam, c.nv, c.nu, m.rmax, m.g, steps, entry, \
                    mu_int, proj, y, acc, stats
 
 // 4 resident 128-thread blocks per SM (128 registers, no spills).  Capping the
