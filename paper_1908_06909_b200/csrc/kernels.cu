@@ -852,11 +852,6 @@ cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry, voi
     return cudaGetLastError();
 }
 
-static dim3 trace_grid(const LaunchChunk& c) {
-    const unsigned tiles = (unsigned)(((c.nu + 15) / 16) * ((c.nv + 7) / 8));
-    return dim3(tiles, (unsigned)c.n_angles);
-}
-
 // Warp pixel tile of the exact walker: (1 << tw_log) x (32 >> tw_log); default
 // 8 x 4 (TETPROJ_TILE_W overrides for measurements).
 static int tile_w_log() {
