@@ -79,6 +79,17 @@ def test_c4b_jittered_slivers():
     U.check_parity(w.mesh, w.geom, w.mu, w.y)
 
 
+def test_wide_cone_generic_frame():
+    """Huge pixels: a 16x8 tile's rays spread over >45 degrees, so the block
+    vote rejects every fixed shear axis and the generic per-ray frame runs."""
+    m = M.ball_mesh(h=0.2, seed=2)
+    geom = G.circular_cone(G.equidistant(3) + 0.4, 3.0, 4.5, 24, 20, 0.6, 0.6)
+    rng = np.random.default_rng(4)
+    mu = rng.uniform(0.2, 1.0, m.n_tets).astype(np.float32)
+    y = rng.uniform(0.5, 1.5, geom.n_rays).astype(np.float32)
+    U.check_parity(m, geom, mu, y)
+
+
 def test_empty_detector_misses_mesh():
     m = M.ball_mesh(h=0.3, seed=3)
     geom = G.circular_cone([0.0], 4.0, 8.0, 8, 8, 0.1, 0.1, off_u=200.0)
