@@ -12,7 +12,6 @@ Prints one JSON object; copied to profiles/ as rNN_microbench.json.
 import ctypes as C
 import json
 import os
-import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -21,9 +20,9 @@ LIB = os.path.join(ROOT, "paper_1908_06909_b200", "libtetmicro.so")
 
 
 def build():
-    if not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        subprocess.check_call(["nvcc", "-O3", "-gencode", "arch=compute_100a,code=sm_100a",
-                               "-Xcompiler", "-fPIC", "-shared", SRC, "-o", LIB])
+    sys.path.insert(0, ROOT)
+    from paper_1908_06909_b200 import _build
+    _build.build_micro()
     L = C.CDLL(LIB)
     L.tetmicro_run.argtypes = [C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_int]
     L.tetmicro_run.restype = C.c_double

@@ -30,6 +30,20 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+MICRO_SRC = os.path.join(CSRC, "microbench.cu")
+MICRO_LIB = os.path.join(HERE, "libtetmicro.so")
+
+
+def build_micro(force: bool = False) -> str:
+    """libtetmicro.so: roofline microbenchmarks (experiments/microbench.py)."""
+    if force or not os.path.exists(MICRO_LIB) or os.path.getmtime(MICRO_LIB) < os.path.getmtime(MICRO_SRC):
+        tmp = MICRO_LIB + f".tmp{os.getpid()}"
+        subprocess.check_call([nvcc(), "-O3", "-gencode", "arch=compute_100a,code=sm_100a",
+                               "-lineinfo", "-Xcompiler", "-fPIC", "-shared", MICRO_SRC, "-o", tmp])
+        os.replace(tmp, MICRO_LIB)
+    return MICRO_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB

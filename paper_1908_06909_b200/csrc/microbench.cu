@@ -32,15 +32,22 @@ __global__ void gather32_kernel(const int4* __restrict__ buf, uint64_t n_rec, in
     if (acc == 0x12345678u) sink[0] = acc;
 }
 
+// Coalesced reads; in pass r block b reads the slice of block (b + 37 r) so no
+// SM re-reads its own slice from L1 (the buffer is L2-resident, not L1).
 __global__ void stream_kernel(const int4* __restrict__ buf, uint64_t n16, int reps,
                               unsigned* __restrict__ sink) {
     unsigned acc = 0;
-    for (int r = 0; r < reps; ++r)
-        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16;
-             i += (uint64_t)gridDim.x * blockDim.x) {
-            const int4 v = __ldg(buf + i);
+    const uint64_t per = (n16 + gridDim.x - 1) / gridDim.x;
+    for (int r = 0; r < reps; ++r) {
+        const uint64_t blk = (blockIdx.x + 37ull * r) % gridDim.x;
+        const uint64_t lo = blk * per, hi = lo + per < n16 ? lo + per : n16;
+        for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+            int4 v;
+            asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(buf + i));
             acc += v.x ^ v.y ^ v.z ^ v.w;
         }
+    }
     if (acc == 0x12345678u) sink[0] = acc;
 }
 
