@@ -332,6 +332,21 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     m->dev.g = H.g;
     m->dev.rmax = H.rmax;
     for (int i = 0; i < 3; ++i) m->dev.C[i] = H.C[i];
+    {   // L2 persistence for the face tags (TETPROJ_L2_PERSIST=1): carve out the
+        // device's persisting L2 and size the window to the records
+        const char* ev = std::getenv("TETPROJ_L2_PERSIST");
+        if (ev && ev[0] == '1') {
+            int max_persist = 0, max_window = 0;
+            cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+            cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
+            const size_t rec_bytes = (size_t)H.nt * 32;
+            if (max_persist > 0 && max_window > 0) {
+                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+                m->dev.l2_window_bytes = std::min(rec_bytes, (size_t)max_window);
+                m->dev.l2_hit_ratio = std::min(1.0, (double)max_persist / (double)m->dev.l2_window_bytes);
+            }
+        }
+    }
     // host copies are no longer needed
     std::vector<int32_t>().swap(H.rec);
     std::vector<int32_t>().swap(H.tnode);
@@ -423,7 +438,7 @@ tet_status tet_mesh_info(tet_mesh_t m, int64_t info[8]) {
     info[3] = m->device;
     info[4] = m->host.e;
     info[5] = m->bytes;
-    info[6] = 0;
+    info[6] = (int64_t)m->dev.l2_window_bytes;
     info[7] = m->host.reordered ? 1 : 0;
     return TET_OK;
 }

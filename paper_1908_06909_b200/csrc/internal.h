@@ -65,6 +65,8 @@ struct DevMesh {
     int64_t nv = 0, nt = 0, nb = 0;
     double g = 0, rmax = 0;
     double C[3] = {0, 0, 0};     // grid origin (world units)
+    size_t l2_window_bytes = 0;  // L2 persistence window over rec (0 = off)
+    double l2_hit_ratio = 0;
 };
 
 struct MtOptions {

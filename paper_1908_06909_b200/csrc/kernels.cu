@@ -881,7 +881,26 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
                          unsigned long long* stats, cudaStream_t s) {
     const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
     const int twl = tile_w_log();
-    trace_kernel<BACK, 4><<<trace_grid_w(c, twl), 128, 0, s>>>(TRACE_ARGS, twl);
+    if (m.l2_window_bytes == 0) {
+        trace_kernel<BACK, 4><<<trace_grid_w(c, twl), 128, 0, s>>>(TRACE_ARGS, twl);
+        return;
+    }
+    // L2 persistence hint for the face-tag records (per launch; the caller's
+    // stream attributes are not touched): hits persist, misses stream.
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = trace_grid_w(c, twl);
+    cfg.blockDim = dim3(128);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = (void*)m.rec;
+    attr[0].val.accessPolicyWindow.num_bytes = m.l2_window_bytes;
+    attr[0].val.accessPolicyWindow.hitRatio = (float)m.l2_hit_ratio;
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, trace_kernel<BACK, 4>, TRACE_ARGS, twl);
 }
 
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
