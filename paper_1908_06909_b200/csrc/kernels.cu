@@ -582,218 +582,6 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
         }
     }
 
-// ---- two rays per thread (trace2_kernel) ---------------------------------
-// The same walk as walk_ray, as a struct whose step() has no early exit: a
-// thread advances two rays in lockstep, so the two independent dependency
-// chains interleave (ILP) and the per-thread overhead registers are shared.
-// A finished ray stays inactive (its side effects are masked) until the other
-// one finishes.
-struct WalkCtx {
-    const int4* __restrict__ rec;
-    const int4* __restrict__ tnode;
-    const int4* __restrict__ vtx;
-    const AngleGeom* __restrict__ ang;
-    const float* __restrict__ mu;
-    const float* __restrict__ y;
-    double* __restrict__ acc;
-    double rmax, g;
-    int beam, max_steps;
-};
-
-template <bool BACK, int AX>
-struct Walker {
-    Frame F;
-    int a, u, v;
-    float yv, mut;
-    int t, kin, lp, id0, id1, id2, iap, steps_left;
-    double x0, y0, z0, x1, y1, z1, x2, y2, z2, s01, s12, s20, zin, sum;
-    int4 ta, tb, X;
-    bool active;
-
-    __device__ __forceinline__ void init(const WalkCtx& c, int a_, int u_, int v_, int e,
-                                         size_t rid) {
-        a = a_; u = u_; v = v_;
-        sum = 0.0;
-        active = e >= 0;
-        if (!active) e = 0;   // valid dummy state (tet 0) for the masked lockstep
-        const RayPts r = ray_points(c.ang[a], c.beam, u, v);
-        make_frame_ax<AX>(r, c.rmax, c.g, F);
-        yv = (BACK && active) ? c.y[rid] : 0.f;
-        t = e >> 2;
-        kin = e & 3;
-        const int4 nodes = __ldg(c.tnode + t);
-        if (kin == 0)      { id0 = nodes.y; id1 = nodes.z; id2 = nodes.w; lp = 1 | 2 << 2 | 3 << 4; }
-        else if (kin == 1) { id0 = nodes.x; id1 = nodes.w; id2 = nodes.z; lp = 0 | 3 << 2 | 2 << 4; }
-        else if (kin == 2) { id0 = nodes.x; id1 = nodes.y; id2 = nodes.w; lp = 0 | 1 << 2 | 3 << 4; }
-        else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; lp = 0 | 2 << 2 | 1 << 4; }
-        iap = sel4(nodes, kin);
-        xform_ax<AX>(F, __ldg(c.vtx + id0), x0, y0, z0);
-        xform_ax<AX>(F, __ldg(c.vtx + id1), x1, y1, z1);
-        xform_ax<AX>(F, __ldg(c.vtx + id2), x2, y2, z2);
-        s01 = side2(x0, y0, x1, y1);
-        s12 = side2(x1, y1, x2, y2);
-        s20 = side2(x2, y2, x0, y0);
-        const double w0 = fabs(s12), w1 = fabs(s20), w2 = fabs(s01);
-        const double sw = w0 + w1 + w2;
-        zin = sw > 0 ? (w0 * z0 + w1 * z1 + w2 * z2) / sw : (z0 + z1 + z2) * (1.0 / 3.0);
-        steps_left = c.max_steps;
-        ldg_rec256(c.rec + 2 * (size_t)t, ta, tb);
-        mut = BACK ? 0.f : __ldg(c.mu + t);
-        X = __ldg(c.vtx + iap);
-    }
-
-    __device__ __forceinline__ void step(const WalkCtx& c, unsigned& n_cross, unsigned& n_exact,
-                                         unsigned& n_lost, unsigned& n_stuck) {
-        double x3, y3, z3;
-        xform_ax<AX>(F, X, x3, y3, z3);
-        const double p0 = side2(x3, y3, x0, y0);
-        const double p1 = side2(x3, y3, x1, y1);
-        const double p2 = side2(x3, y3, x2, y2);
-        bool n0 = p0 < -F.tau, n1 = p1 < -F.tau, n2 = p2 < -F.tau;
-        const bool u0 = !n0 && !(p0 > F.tau), u1 = !n1 && !(p1 > F.tau), u2 = !n2 && !(p2 > F.tau);
-        if (active && (u0 | u1 | u2)) {
-            if (u0) { n0 = exact_side_ids(c.vtx, c.ang, c.beam, a, u, v, iap, id0) < 0; ++n_exact; }
-            if (u1) { n1 = exact_side_ids(c.vtx, c.ang, c.beam, a, u, v, iap, id1) < 0; ++n_exact; }
-            if (u2) { n2 = exact_side_ids(c.vtx, c.ang, c.beam, a, u, v, iap, id2) < 0; ++n_exact; }
-        }
-        const bool c0 = n0 && !n1;
-        const bool c1 = n1 && !n2 && !c0;
-        n_lost += (active && n0 == n1 && n1 == n2) ? 1u : 0u;
-        const int j = selp(2, selp(0, 1, c1), c0);
-        const int L = (lp >> (2 * j)) & 3;
-        const int lo = selp(selp(ta.x, ta.z, L == 0), selp(tb.x, tb.z, L == 2), L < 2);
-        const unsigned hi = (unsigned)selp(selp(ta.y, ta.w, L == 0), selp(tb.y, tb.w, L == 2), L < 2);
-        const bool more = active && lo >= 0 && --steps_left != 0;
-        const int tcur = t;
-        const float mcur = mut;
-        const bool d0 = j == 0, d1 = j == 1, d2 = j == 2;
-        if (more) {
-            t = lo >> 2;
-            ldg_rec256(c.rec + 2 * (size_t)t, ta, tb);
-            if (!BACK) mut = __ldg(c.mu + t);
-            X = __ldg(c.vtx + (int)(hi >> 8));
-            const int q0 = selp(kin, lp & 3, d0);
-            const int q1 = selp(kin, (lp >> 2) & 3, d1);
-            const int q2 = selp(kin, (lp >> 4) & 3, d2);
-            lp = ((hi >> (2 * q0)) & 3) | (((hi >> (2 * q1)) & 3) << 2) | (((hi >> (2 * q2)) & 3) << 4);
-            kin = lo & 3;
-        }
-        double si = s20, pi = p2, pn = p0, zi = z2, zn = z0;
-        if (c0) { si = s01; pi = p0; pn = p1; zi = z0; zn = z1; }
-        if (c1) { si = s12; pi = p1; pn = p2; zi = z1; zn = z2; }
-        const double wA = fabs(si), wQ = fabs(pn), wR = fabs(pi);
-        const double sw = wA + wQ + wR;
-        const double zout = sw > 0.0 ? fma(fma(wQ, zi - z3, wR * (zn - z3)), rcp_nr(sw), z3) : zin;
-        const double chord = (zout - zin) * F.scale;
-        if (active) {
-            if (BACK) {
-                if (chord > 0.0) atomicAdd(c.acc + tcur, chord * (double)yv);
-            } else {
-                sum = fma(chord, (double)mcur, sum);
-            }
-            ++n_cross;
-            if (!more && lo >= 0) ++n_stuck;
-        }
-        if (more) {
-            if (d0) { x0 = x3; y0 = y3; z0 = z3; id0 = iap; s20 = -p2; s01 = p1; }
-            if (d1) { x1 = x3; y1 = y3; z1 = z3; id1 = iap; s01 = -p0; s12 = p2; }
-            if (d2) { x2 = x3; y2 = y3; z2 = z3; id2 = iap; s12 = -p1; s20 = p0; }
-            zin = zout;
-            iap = (int)(hi >> 8);
-        }
-        active = more;
-    }
-};
-
-template <bool BACK, int AX>
-__device__ __forceinline__ void walk_pair(const WalkCtx& c, int a, int uA, int vA, int eA,
-                                          size_t ridA, int uB, int vB, int eB, size_t ridB,
-                                          double& sumA, double& sumB, unsigned& n_cross,
-                                          unsigned& n_exact, unsigned& n_lost, unsigned& n_stuck) {
-    Walker<BACK, AX> A, B;
-    A.init(c, a, uA, vA, eA, ridA);
-    B.init(c, a, uB, vB, eB, ridB);
-    while (A.active || B.active) {
-        A.step(c, n_cross, n_exact, n_lost, n_stuck);
-        B.step(c, n_cross, n_exact, n_lost, n_stuck);
-    }
-    sumA = A.sum;
-    sumB = B.sum;
-}
-
-// Two rays per thread: warp = 8x8 pixels (ray A in rows 0-3, ray B in rows
-// 4-7 of the warp tile), block = 2x2 warps = 16x16 pixels.
-template <bool BACK>
-__global__ void __launch_bounds__(128, 2) trace2_kernel(const int4* __restrict__ rec,
-                                                       const int4* __restrict__ tnode,
-                                                       const int4* __restrict__ vtx,
-                                                       const AngleGeom* __restrict__ ang,
-                                                       int beam, int nv, int nu, double rmax,
-                                                       double g, int max_steps,
-                                                       const int* __restrict__ entry,
-                                                       const float* __restrict__ mu,
-                                                       float* __restrict__ proj,
-                                                       const float* __restrict__ y,
-                                                       double* __restrict__ acc,
-                                                       unsigned long long* __restrict__ stats) {
-    const int tiles_u = (nu + 15) >> 4;
-    const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
-    const int a = blockIdx.y;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int u = bx * 16 + (w & 1) * 8 + (lane & 7);
-    const int vA = by * 16 + (w >> 1) * 8 + (lane >> 3), vB = vA + 4;
-    const bool validA = u < nu && vA < nv, validB = u < nu && vB < nv;
-    const size_t ridA = ((size_t)a * nv + vA) * nu + u, ridB = ((size_t)a * nv + vB) * nu + u;
-    const int eA = validA ? entry[ridA] : -1, eB = validB ? entry[ridB] : -1;
-    unsigned n_cross = 0, n_exact = 0, n_lost = 0, n_stuck = 0;
-    double sumA = 0.0, sumB = 0.0;
-    int ax = 6;
-    {
-        const int uc = min(bx * 16 + 8, nu - 1), vc = min(by * 16 + 8, nv - 1);
-        const RayPts rc = ray_points(ang[a], beam, uc, vc);
-        const long long cx = rc.px - rc.ox, cy = rc.py - rc.oy, cz = rc.pz - rc.oz;
-        const long long ax_ = cx < 0 ? -cx : cx, ay_ = cy < 0 ? -cy : cy, az_ = cz < 0 ? -cz : cz;
-        const int kc = (ax_ >= ay_ && ax_ >= az_) ? 0 : (ay_ >= az_ ? 1 : 2);
-        const long long dkc = kc == 0 ? cx : (kc == 1 ? cy : cz);
-        bool ok = true;
-        for (int r2 = 0; r2 < 2; ++r2) {
-            const int vv = r2 ? vB : vA;
-            if ((r2 ? eB : eA) < 0) continue;
-            const RayPts r = ray_points(ang[a], beam, u, vv);
-            const long long dx = r.px - r.ox, dy = r.py - r.oy, dz = r.pz - r.oz;
-            const long long dk = kc == 0 ? dx : (kc == 1 ? dy : dz);
-            const long long adk = dk < 0 ? -dk : dk;
-            const long long m = max(dx < 0 ? -dx : dx, max(dy < 0 ? -dy : dy, dz < 0 ? -dz : dz));
-            ok = ok && (dk < 0) == (dkc < 0) && 2 * adk >= m;
-        }
-        if (__syncthreads_and(ok)) ax = 2 * kc + (dkc < 0 ? 1 : 0);
-    }
-    if (eA >= 0 || eB >= 0) {
-        const WalkCtx c{rec, tnode, vtx, ang, mu, y, acc, rmax, g, beam, max_steps};
-#define WALK2(AXV) walk_pair<BACK, AXV>(c, a, u, vA, eA, ridA, u, vB, eB, ridB, sumA, sumB, \
-                                        n_cross, n_exact, n_lost, n_stuck)
-        switch (ax) {
-            case 0: WALK2(0); break;
-            case 1: WALK2(1); break;
-            case 2: WALK2(2); break;
-            case 3: WALK2(3); break;
-            case 4: WALK2(4); break;
-            case 5: WALK2(5); break;
-            default: WALK2(6); break;
-        }
-#undef WALK2
-    }
-    if (!BACK) {
-        if (validA) proj[ridA] = (float)sumA;
-        if (validB) proj[ridB] = (float)sumB;
-    }
-    add_stat(stats, ST_HIT, (eA >= 0 ? 1u : 0u) + (eB >= 0 ? 1u : 0u));
-    add_stat(stats, ST_CROSS, n_cross);
-    add_stat(stats, ST_EXACT, n_exact);
-    add_stat(stats, ST_LOST, n_lost);
-    add_stat(stats, ST_STUCK, n_stuck);
-}
-
 template <bool BACK, int MINB>
 __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict__ rec,
                                                           const int4* __restrict__ tnode,
@@ -1092,17 +880,6 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
                          const float* mu_int, float* proj, const float* y, double* acc,
                          unsigned long long* stats, cudaStream_t s) {
     const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
-    static const bool pair = [] {
-        const char* e = getenv("TETPROJ_PAIR");
-        return e && e[0] == '1';
-    }();
-    if (pair) {
-        const dim3 grid((unsigned)(((c.nu + 15) / 16) * ((c.nv + 15) / 16)), (unsigned)c.n_angles);
-        trace2_kernel<BACK><<<grid, 128, 0, s>>>(m.rec, m.tnode, m.vtx, c.ang, c.beam, c.nv, c.nu,
-                                                 m.rmax, m.g, steps, entry, mu_int, proj, y, acc,
-                                                 stats);
-        return;
-    }
     const int twl = tile_w_log();
     if (m.l2_window_bytes == 0) {
         trace_kernel<BACK, 4><<<trace_grid_w(c, twl), 128, 0, s>>>(TRACE_ARGS, twl);
