@@ -1,17 +1,20 @@
 // kernels.cu -- sm_100a kernels of libtetproj.
 //
-//   entry_kernel      hull-entry finder: per (hull face,
-//                     angle) block, exact test of every pixel in the face's
-//                     detector footprint; writes entry[ray] = tet<<2 | k.
+//   entry_setup_kernel / entry_raster_kernel
+//                     hull-entry finder: per (hull face,
+//                     angle) item, exact affine side coefficients, then an
+//                     exact test of every pixel in the face's detector
+//                     footprint; writes entry[ray] = tet<<2 | k.
 //   trace_kernel<B,M> ray walk (a4) + forward accumulate (a5, B=false) or
 //                     backprojection scatter (a6, B=true).  Alg. 2 of the
 //                     paper with exact sign decisions.
+//   mt_trace_kernel   the paper's own epsilon-MT traversal (NEXT-1 study).
 //   gather / scatter  caller order <-> internal SFC order (K4).
 //
 // Exactness (R2-R4): side(a,b) = sign det[a-o, b-o, p-o] on the
 // integer grid, symbolically perturbed.  The hot loop evaluates it in fp64
-// in a per-ray orthonormal frame (2 FMAs per side) and certifies the sign
-// with a static error bound tau; only |side| <= tau falls back to an int128
+// in a per-ray shear frame (2 FMAs per side) and certifies the sign with a
+// static error bound tau; only |side| <= tau falls back to an int128
 // evaluation of the determinant and the 9-term SoS table.
 #include <cuda_runtime.h>
 #include <stdint.h>
