@@ -218,7 +218,10 @@ def main():
     w, full_geom, geom, y_np = rank_workload(args.config, rank, ws, args.angles)
     if ws > 1 and rank == 0:
         dist.barrier()
-    tm = T.TetMesh.from_mesh(w.mesh, device=local)
+    torch.cuda.synchronize()
+    t_create = time.perf_counter()
+    tm = T.TetMesh.from_mesh(w.mesh, device=local)   # validate, snap, reorder, upload
+    t_create = time.perf_counter() - t_create
     h = tm.handle
     mu = torch.from_numpy(w.mu).to(dev)
     y = torch.from_numpy(y_np).to(dev)
@@ -325,7 +328,8 @@ def main():
             dom, bytes_unit, cross_unit, launches, tdom = "forward", BYTES_FWD, st_f["crossings"], nf, tf
         algo_bytes_per_launch = bytes_unit * cross_unit / max(launches // args.steps, 1)
         achieved = algo_bytes_per_launch / (tdom / max(launches, 1) / 1e3) / 1e9
-        n_launch_step = (nf + nb + ne + np_) / args.steps
+        # each timed entry region launches two kernels (setup + raster)
+        n_launch_step = (nf + nb + 2 * ne + np_) / args.steps
         clk = clocks.summary()
         line = {
             "metric": METRIC,
@@ -355,6 +359,7 @@ def main():
             "stuck": st_f["stuck"] + st_b["stuck"],
             "exact_fallbacks_per_step": st_f["exact_fallbacks"] + st_b["exact_fallbacks"],
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
+            "mesh_create_s": t_create,
             "roofline": {"bound": "hbm", "kernel": f"trace_kernel<{dom}>",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
