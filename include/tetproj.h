@@ -104,11 +104,21 @@ typedef struct {
  * escalation exceeds max_escalations are counted as `lost` and contribute what
  * was summed so far; walks longer than n_tets steps are `stuck`.             */
 enum { TET_TRAVERSE_EXACT = 0, TET_TRAVERSE_MT_F64 = 1, TET_TRAVERSE_MT_F32 = 2 };
+/* Entry finder (the "index of a tetrahedron on the mesh boundary" each ray
+ * starts from):
+ *   TET_ENTRY_RASTER : per (hull face, angle) exact rasterisation of the face's
+ *                      detector footprint (default)
+ *   TET_ENTRY_BVH    : per-ray search of a BVH over the hull faces (the
+ *                      paper's tree-search approach, binary BVH for R*-tree)
+ * Both take the same exact entering decision, so results are identical.     */
+enum { TET_ENTRY_RASTER = 0, TET_ENTRY_BVH = 1 };
 typedef struct {
     int32_t traversal;         /* TET_TRAVERSE_*                                 */
     int32_t max_escalations;   /* MT modes: 12 (SPEC.md:314 reading)            */
     double eps0;               /* MT modes: 1e-9 ("eps <- 10^-9")  */
     double eps_growth;         /* MT modes: 10 ("eps <- eps*10")   */
+    int32_t entry;             /* TET_ENTRY_*                                    */
+    int32_t _reserved;
 } tet_options;
 
 /* Create a mesh on CUDA device `device` (§2.2 graph + boundary list).

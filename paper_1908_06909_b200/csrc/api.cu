@@ -23,6 +23,8 @@ struct tet_mesh {
     void* d_vtx = nullptr;
     void* d_hull = nullptr;
     void* d_perm = nullptr;
+    void* d_bvh_nodes = nullptr;
+    void* d_bvh_faces = nullptr;
     int64_t bytes = 0;
     // kernel timing (tet_set_kernel_timing)
     struct TimerRec { int kind; cudaEvent_t a, b; };
@@ -149,6 +151,9 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
                Op op, void* stream, tet_stats* st, const tet_options* opt = nullptr) {
     if (!m) return fail(TET_E_ARG, "null mesh");
     const int mode = opt ? opt->traversal : TET_TRAVERSE_EXACT;
+    const int entry_mode = opt ? opt->entry : TET_ENTRY_RASTER;
+    if (entry_mode != TET_ENTRY_RASTER && entry_mode != TET_ENTRY_BVH)
+        return fail(TET_E_ARG, "unknown entry finder");
     if (mode < TET_TRAVERSE_EXACT || mode > TET_TRAVERSE_MT_F32)
         return fail(TET_E_ARG, "unknown traversal mode");
     MtOptions mto;
@@ -230,7 +235,10 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
             CU(cudaMemsetAsync(entry, 0xff, sizeof(int) * per_angle * na, s));
             {
                 KernelTimer kt(m, TET_K_ENTRY, s);
-                CU(launch_entry(m->dev, c, entry, entry_scratch, d_stats, s));
+                if (entry_mode == TET_ENTRY_BVH)
+                    CU(launch_entry_bvh(m->dev, c, entry, d_stats, s));
+                else
+                    CU(launch_entry(m->dev, c, entry, entry_scratch, d_stats, s));
             }
             const size_t off = (size_t)a0 * per_angle;
             const bool fwd = op == Op::Forward;
@@ -317,6 +325,8 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     if (e == cudaSuccess) e = up(&m->d_vtx, H.vtx.data(), H.vtx.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_hull, H.hull.data(), H.hull.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_perm, H.perm.data(), H.perm.size() * 4);
+    if (e == cudaSuccess) e = up(&m->d_bvh_nodes, H.bvh_nodes.data(), H.bvh_nodes.size() * 4);
+    if (e == cudaSuccess) e = up(&m->d_bvh_faces, H.bvh_faces.data(), H.bvh_faces.size() * 4);
     if (e != cudaSuccess) {
         tet_mesh_destroy(m);
         return cuda_fail(e, "tet_mesh_create upload");
@@ -326,6 +336,8 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     m->dev.vtx = (const int4*)m->d_vtx;
     m->dev.hull = (const int2*)m->d_hull;
     m->dev.perm = (const int*)m->d_perm;
+    m->dev.bvh_nodes = (const int4*)m->d_bvh_nodes;
+    m->dev.bvh_faces = (const int4*)m->d_bvh_faces;
     m->dev.nv = H.nv;
     m->dev.nt = H.nt;
     m->dev.nb = H.nb;
@@ -353,6 +365,8 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     std::vector<int32_t>().swap(H.vtx);
     std::vector<int32_t>().swap(H.hull);
     std::vector<int32_t>().swap(H.perm);
+    std::vector<int32_t>().swap(H.bvh_nodes);
+    std::vector<int32_t>().swap(H.bvh_faces);
     *out = m;
     return TET_OK;
 }
@@ -370,6 +384,8 @@ tet_status tet_mesh_destroy(tet_mesh_t m) {
     cudaFree(m->d_vtx);
     cudaFree(m->d_hull);
     cudaFree(m->d_perm);
+    cudaFree(m->d_bvh_nodes);
+    cudaFree(m->d_bvh_faces);
     delete m;
     return TET_OK;
 }

@@ -39,6 +39,8 @@ struct HostMesh {
     std::vector<int32_t> tnode;// [T][4] vertex ids (ray initialisation, entry finder)
     std::vector<int32_t> hull; // [B][2] (t, k) internal order
     std::vector<int32_t> perm; // [T] internal -> caller tet index
+    std::vector<int32_t> bvh_nodes;  // [N][8] float lo[3], hi[3] | left, right (leaf: -(first+1), count)
+    std::vector<int32_t> bvh_faces;  // [B][4] vertex ids (outward order) | entry code tet<<2|k
     double rmax = 0;           // max |X|_2 over vertices (grid units)
     double bs_c[3] = {0, 0, 0}, bs_r = 0;  // bounding sphere (grid units)
     bool reordered = false;
@@ -62,6 +64,8 @@ struct DevMesh {
     const int4* vtx = nullptr;   // [V]
     const int2* hull = nullptr;  // [B]
     const int* perm = nullptr;   // [T]
+    const int4* bvh_nodes = nullptr;  // [2N] hull-face BVH (TET_ENTRY_BVH)
+    const int4* bvh_faces = nullptr;  // [B]
     int64_t nv = 0, nt = 0, nb = 0;
     double g = 0, rmax = 0;
     double C[3] = {0, 0, 0};     // grid origin (world units)
@@ -89,6 +93,8 @@ struct LaunchChunk {
 size_t entry_scratch_bytes(const DevMesh& m, int n_angles);
 cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry, void* scratch,
                          unsigned long long* stats, cudaStream_t s);
+cudaError_t launch_entry_bvh(const DevMesh& m, const LaunchChunk& c, int* entry,
+                             unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
                            const float* mu_int, float* proj, unsigned long long* stats,
                            cudaStream_t s);

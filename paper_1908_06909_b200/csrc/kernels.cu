@@ -437,6 +437,76 @@ __global__ void __launch_bounds__(128, 8) entry_raster_kernel(
     if (exact) atomicAdd(stats + ST_EXACT, (unsigned long long)exact);
 }
 
+// Alternative entry finder (TET_ENTRY_BVH; NEXT-3): one thread per ray walks
+// a BVH over the hull faces (the paper's per-ray tree search, PAPER.md:154-158,
+// with a binary BVH instead of an R*-tree).  Boxes are float, rounded
+// outward, tested in fp64 with a margin, so they never prune a face the ray
+// meets; the entering test at the leaves is exact, and because the entering
+// face is unique the search stops at the first one found.
+__global__ void __launch_bounds__(128) entry_bvh_kernel(const int4* __restrict__ nodes,
+                                                        const int4* __restrict__ faces,
+                                                        const int4* __restrict__ vtx,
+                                                        const AngleGeom* __restrict__ ang,
+                                                        int beam, int nv, int nu,
+                                                        int* __restrict__ entry,
+                                                        unsigned long long* __restrict__ stats) {
+    const int tiles_u = (nu + 15) >> 4;
+    const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
+    const int a = blockIdx.y;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int u = bx * 16 + (w & 1) * 8 + (lane & 7);
+    const int v = by * 8 + (w >> 1) * 4 + (lane >> 3);
+    unsigned exact = 0;
+    if (u < nu && v < nv) {
+        const RayPts r = ray_points(ang[a], beam, u, v);
+        const double o[3] = {(double)r.ox, (double)r.oy, (double)r.oz};
+        const double d[3] = {(double)(r.px - r.ox), (double)(r.py - r.oy), (double)(r.pz - r.oz)};
+        double inv[3];
+        for (int i = 0; i < 3; ++i) inv[i] = 1.0 / d[i];   // +-inf for d = 0
+        int stack[64];
+        int sp = 0, found = -1;
+        stack[sp++] = 0;
+        while (sp > 0 && found < 0) {
+            const int n = stack[--sp];
+            const int4 q0 = __ldg(nodes + 2 * n), q1 = __ldg(nodes + 2 * n + 1);
+            const float lo[3] = {__int_as_float(q0.x), __int_as_float(q0.y), __int_as_float(q0.z)};
+            const float hi[3] = {__int_as_float(q0.w), __int_as_float(q1.x), __int_as_float(q1.y)};
+            double tmin = -INFINITY, tmax = INFINITY;
+            bool miss = false;
+            for (int i = 0; i < 3; ++i) {
+                const double m = 2.0 + 1e-9 * (fabs((double)lo[i]) + fabs(o[i]));
+                const double l = (double)lo[i] - m, h = (double)hi[i] + m;
+                if (d[i] == 0.0) {
+                    miss |= o[i] < l || o[i] > h;
+                } else {
+                    const double t1 = (l - o[i]) * inv[i], t2 = (h - o[i]) * inv[i];
+                    tmin = fmax(tmin, fmin(t1, t2));
+                    tmax = fmin(tmax, fmax(t1, t2));
+                }
+            }
+            if (miss || tmin > tmax + 1e-9 * (fabs(tmin) + fabs(tmax))) continue;
+            if (q1.z < 0) {   // leaf
+                const int first = -q1.z - 1, cnt = q1.w;
+                for (int f = first; f < first + cnt; ++f) {
+                    const int4 fc = __ldg(faces + f);
+                    const int4 A = __ldg(vtx + fc.x), B = __ldg(vtx + fc.y), C = __ldg(vtx + fc.z);
+                    if (side_direct(A, B, r, exact) == -1 && side_direct(B, C, r, exact) == -1 &&
+                        side_direct(C, A, r, exact) == -1) {
+                        found = fc.w;
+                        break;
+                    }
+                }
+            } else if (sp < 62) {
+                stack[sp++] = q1.w;
+                stack[sp++] = q1.z;
+            }
+        }
+        if (found >= 0) entry[((size_t)a * nv + v) * nu + u] = found;
+    }
+    const unsigned s = __reduce_add_sync(0xffffffffu, exact);
+    if (lane == 0 && s) atomicAdd(stats + ST_EXACT, (unsigned long long)s);
+}
+
 // ------------------------------------------------------------ walker ----
 // Certified sign of a side value (filter, else exact int128 + SoS).
 #define SIGN_OF(val, id_other, out)                                                   \
@@ -842,6 +912,14 @@ static int grid_for(int64_t n) {
 // ----------------------------------------------------------- launchers --
 size_t entry_scratch_bytes(const DevMesh& m, int n_angles) {
     return sizeof(EntryItem) * (size_t)m.nb * n_angles + 256;
+}
+
+cudaError_t launch_entry_bvh(const DevMesh& m, const LaunchChunk& c, int* entry,
+                             unsigned long long* stats, cudaStream_t s) {
+    const dim3 grid((unsigned)(((c.nu + 15) / 16) * ((c.nv + 7) / 8)), (unsigned)c.n_angles);
+    entry_bvh_kernel<<<grid, 128, 0, s>>>(m.bvh_nodes, m.bvh_faces, m.vtx, c.ang, c.beam, c.nv,
+                                          c.nu, entry, stats);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry, void* scratch,

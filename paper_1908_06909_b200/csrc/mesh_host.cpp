@@ -4,6 +4,7 @@
 // in a pre-processing step").
 #include <algorithm>
 #include <cmath>
+#include <climits>
 #include <cstring>
 #include <numeric>
 #include <unordered_map>
@@ -69,6 +70,104 @@ uint64_t spread21(uint64_t x) {
     x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
     x = (x | x << 2) & 0x1249249249249249ULL;
     return x;
+}
+
+// BVH over the hull faces for the per-ray entry finder (TET_ENTRY_BVH):
+// faces sorted by the Morton code of their centroid, complete binary tree by
+// median split, <= 4 faces per leaf, float boxes rounded outward (the boxes
+// only prune; the entering decision is exact at the leaves).
+void build_hull_bvh(HostMesh& M, const std::vector<int32_t>& P, const std::vector<int32_t>& T,
+                    const std::vector<std::pair<int32_t, int>>& hull,
+                    const std::vector<int32_t>& vnew) {
+    const int64_t B = (int64_t)hull.size();
+    struct Face { float lo[3], hi[3]; uint64_t key; int32_t v[3]; };
+    std::vector<Face> f(B);
+    long long mn[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX}, mx[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
+    for (int64_t h = 0; h < B; ++h) {
+        const int t = hull[h].first, k = hull[h].second;
+        for (int j = 0; j < 3; ++j) f[h].v[j] = T[4 * (int64_t)t + kFace[k][j]];
+        for (int i = 0; i < 3; ++i) {
+            long long lo = LLONG_MAX, hi = LLONG_MIN;
+            for (int j = 0; j < 3; ++j) {
+                lo = std::min(lo, (long long)P[3 * f[h].v[j] + i]);
+                hi = std::max(hi, (long long)P[3 * f[h].v[j] + i]);
+            }
+            f[h].lo[i] = std::nextafter((float)lo, -INFINITY);
+            f[h].hi[i] = std::nextafter((float)hi, INFINITY);
+            mn[i] = std::min(mn[i], lo);
+            mx[i] = std::max(mx[i], hi);
+        }
+    }
+    long long span = 1;
+    for (int i = 0; i < 3; ++i) span = std::max(span, mx[i] - mn[i] + 1);
+    int shift = 0;
+    while ((span >> shift) >= (1 << 20)) ++shift;
+    for (int64_t h = 0; h < B; ++h) {
+        uint64_t key = 0;
+        for (int i = 0; i < 3; ++i) {
+            long long c = 0;
+            for (int j = 0; j < 3; ++j) c += P[3 * f[h].v[j] + i];
+            key |= spread21((uint64_t)(((c / 3) - mn[i]) >> shift)) << i;
+        }
+        f[h].key = key;
+    }
+    std::sort(f.begin(), f.end(), [](const Face& a, const Face& b) { return a.key < b.key; });
+    // faces in BVH order: (tet, k) internal + vertex ids
+    M.bvh_faces.resize((size_t)B * 4);
+    for (int64_t h = 0; h < B; ++h)
+        for (int j = 0; j < 3; ++j) M.bvh_faces[4 * h + j] = vnew[f[h].v[j]];
+    // entry code per face: find (t,k) again by matching the face record order
+    {
+        std::unordered_map<uint64_t, int32_t> code;   // sorted-vertex-triple hash -> code
+        code.reserve(B * 2);
+        auto key3 = [](int32_t a, int32_t b, int32_t c) {
+            int32_t x[3] = {a, b, c};
+            std::sort(x, x + 3);
+            return ((uint64_t)(uint32_t)x[0] * 0x9E3779B97F4A7C15ULL) ^ ((uint64_t)(uint32_t)x[1] << 21) ^
+                   ((uint64_t)(uint32_t)x[2] * 0xC2B2AE3D27D4EB4FULL);
+        };
+        for (int64_t h = 0; h < B; ++h) {
+            const int t = hull[h].first, k = hull[h].second;
+            const int32_t a = T[4 * (int64_t)t + kFace[k][0]], b = T[4 * (int64_t)t + kFace[k][1]],
+                          c = T[4 * (int64_t)t + kFace[k][2]];
+            code[key3(a, b, c)] = M.hull[2 * h] * 4 + M.hull[2 * h + 1];
+        }
+        for (int64_t h = 0; h < B; ++h)
+            M.bvh_faces[4 * h + 3] = code[key3(f[h].v[0], f[h].v[1], f[h].v[2])];
+    }
+    // nodes: implicit recursion on [lo, hi) ranges, stored depth-first
+    M.bvh_nodes.clear();
+    struct Rec { int64_t lo, hi, node; };
+    std::vector<Rec> stack;
+    auto push_node = [&]() {
+        M.bvh_nodes.resize(M.bvh_nodes.size() + 8);
+        return (int64_t)(M.bvh_nodes.size() / 8 - 1);
+    };
+    const int64_t root = push_node();
+    stack.push_back({0, B, root});
+    while (!stack.empty()) {
+        Rec r = stack.back();
+        stack.pop_back();
+        float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int64_t h = r.lo; h < r.hi; ++h)
+            for (int i = 0; i < 3; ++i) {
+                lo[i] = std::min(lo[i], f[h].lo[i]);
+                hi[i] = std::max(hi[i], f[h].hi[i]);
+            }
+        float* nd = reinterpret_cast<float*>(&M.bvh_nodes[8 * r.node]);
+        for (int i = 0; i < 3; ++i) { nd[i] = lo[i]; nd[3 + i] = hi[i]; }
+        if (r.hi - r.lo <= 4) {   // leaf: -(first+1), count
+            M.bvh_nodes[8 * r.node + 6] = -(int32_t)(r.lo + 1);
+            M.bvh_nodes[8 * r.node + 7] = (int32_t)(r.hi - r.lo);
+        } else {
+            const int64_t mid = (r.lo + r.hi) / 2;
+            const int64_t L = push_node(), R = push_node();
+            M.bvh_nodes[8 * r.node + 6] = (int32_t)L;
+            M.bvh_nodes[8 * r.node + 7] = (int32_t)R;
+            stack.push_back({mid, r.hi, R});
+            stack.push_back({r.lo, mid, L});
+        }
+    }
 }
 
 }  // namespace
@@ -321,6 +420,7 @@ tet_status prepare_mesh(const double* verts, int64_t nv, const int32_t* tets,
         M.hull[2 * h] = inv[hull[h].first];
         M.hull[2 * h + 1] = hull[h].second;
     }
+    build_hull_bvh(M, P, T, hull, vnew);
     return TET_OK;
 }
 

@@ -53,15 +53,19 @@ class tet_stats(C.Structure):
 TET_TRAVERSE_EXACT, TET_TRAVERSE_MT_F64, TET_TRAVERSE_MT_F32 = 0, 1, 2
 
 
+TET_ENTRY_RASTER, TET_ENTRY_BVH = 0, 1
+
+
 class tet_options(C.Structure):
     _fields_ = [("traversal", C.c_int32), ("max_escalations", C.c_int32), ("eps0", C.c_double),
-                ("eps_growth", C.c_double)]
+                ("eps_growth", C.c_double), ("entry", C.c_int32), ("_reserved", C.c_int32)]
 
 
 def options(traversal: int = TET_TRAVERSE_EXACT, eps0: float = 1e-9, eps_growth: float = 10.0,
-            max_escalations: int = 12) -> tet_options:
-    """Traversal options; MT modes are the paper's Alg. 1/2."""
-    return tet_options(traversal, max_escalations, eps0, eps_growth)
+            max_escalations: int = 12, entry: int = TET_ENTRY_RASTER) -> tet_options:
+    """Traversal / entry-finder options; MT modes are the paper's Alg. 1/2
+    (PAPER.md:79-144), TET_ENTRY_BVH the per-ray tree search."""
+    return tet_options(traversal, max_escalations, eps0, eps_growth, entry, 0)
 
 
 EXPORTS = ["tet_mesh_create", "tet_mesh_destroy", "tet_project", "tet_backproject",

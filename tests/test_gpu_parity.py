@@ -90,6 +90,31 @@ def test_wide_cone_generic_frame():
     U.check_parity(m, geom, mu, y)
 
 
+@pytest.mark.parametrize("case", ["c1", "lattice", "c2"])
+def test_bvh_entry_finder_identical(case):
+    """NEXT-3: the per-ray BVH entry finder takes the same exact decisions as
+    the footprint rasteriser: identical projections and crossing counts."""
+    import torch
+
+    from paper_1908_06909_b200 import tetproj as T
+    if case == "c1":
+        w = CF.workload("c1")
+        mesh, geom, mu = w.mesh, w.geom, w.mu
+    elif case == "lattice":
+        mesh = M.random_small_mesh(40, 2)
+        geom = G.lattice_parallel((1 / 8,) * 3, (0, 0, 0), 19, 13, G.LATTICE_DIRS[:6])
+        mu = np.random.default_rng(1).uniform(0.5, 1.5, mesh.n_tets).astype(np.float32)
+    else:
+        w = CF.workload("c2", n_angles=4, n_u=80, n_v=64)
+        mesh, geom, mu = w.mesh, w.geom, w.mu
+    tm = T.TetMesh.from_mesh(mesh)
+    mu_d = torch.from_numpy(mu).cuda()
+    a, sa = tm.project(geom, mu_d, stats=True)
+    b, sb = tm.project(geom, mu_d, stats=True, opts=T.options(entry=T.TET_ENTRY_BVH))
+    assert torch.equal(a, b)
+    assert sa["crossings"] == sb["crossings"] and sa["rays_hit"] == sb["rays_hit"]
+
+
 def test_empty_detector_misses_mesh():
     m = M.ball_mesh(h=0.3, seed=3)
     geom = G.circular_cone([0.0], 4.0, 8.0, 8, 8, 0.1, 0.1, off_u=200.0)
