@@ -44,6 +44,27 @@ def build_micro(force: bool = False) -> str:
     return MICRO_LIB
 
 
+DEBUG_LIB = os.path.join(HERE, "libtetproj_debug.so")
+
+
+def build_debug(force: bool = False) -> str:
+    """libtetproj_debug.so: the same sources with -DTETPROJ_DEBUG (device-side
+    bounds checks that trap); loaded when TETPROJ_DEBUG_LIB=1."""
+    if force or not os.path.exists(DEBUG_LIB) or any(
+            os.path.getmtime(os.path.join(CSRC, f)) > os.path.getmtime(DEBUG_LIB)
+            for f in SOURCES + HEADERS):
+        tmp = DEBUG_LIB + f".tmp{os.getpid()}"
+        flags = [f for f in NVCC_FLAGS if f not in ("-v", "-Xptxas")]
+        cmd = [nvcc(), *flags, "-DTETPROJ_DEBUG",
+               *[os.path.join(CSRC, f) for f in SOURCES], "-o", tmp]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building libtetproj_debug.so")
+        os.replace(tmp, DEBUG_LIB)
+    return DEBUG_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB

@@ -26,6 +26,15 @@ namespace tetproj {
 
 typedef __int128 i128;
 
+// Debug builds (-DTETPROJ_DEBUG, libtetproj_debug.so) trap on any gathered
+// index outside its array: compute-sanitizer is unavailable on this pool, so
+// the bounds are checked by the kernels themselves.
+#ifdef TETPROJ_DEBUG
+#define DBG_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define DBG_CHECK(cond) do { } while (0)
+#endif
+
 // ------------------------------------------------------------ exact -----
 // Reading R2: sign of det[a-o, b-o, p-o] under o -> o + (d, d^2, d^4),
 // p -> p + (d, d^2, d^4) + (d^8, d^16, d^32): first non-zero of
@@ -430,6 +439,7 @@ __global__ void __launch_bounds__(128, 8) entry_raster_kernel(
         if (sab >= -b0 || sbc >= -b1 || sca >= -b2) {   // a sign the bound cannot certify
             if (!exact_entering(vtx, ang, beam, a, u, v, it->ia, it->ib, it->ic, exact)) continue;
         }
+        DBG_CHECK(u >= 0 && u < nu && v >= 0 && v < nv);
         const int old = atomicExch(entry + ((size_t)a * nv + v) * nu + u, code);
         conflicts += (old != -1);
     }
@@ -527,8 +537,9 @@ template <bool BACK, int AX>
 __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int4* __restrict__ tnode,
                                          const int4* __restrict__ vtx,
                                          const AngleGeom* __restrict__ ang, int beam, int a, int u,
-                                         int v, double rmax, double g, int max_steps, int e,
-                                         size_t rid, const float* __restrict__ mu,
+                                         int v, double rmax, double g, int max_steps,
+                                         int nverts, int e, size_t rid,
+                                         const float* __restrict__ mu,
                                          const float* __restrict__ y, double* __restrict__ acc,
                                          double& sum, unsigned& n_cross, unsigned& n_exact,
                                          unsigned& n_lost, unsigned& n_stuck) {
@@ -537,7 +548,10 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
         make_frame_ax<AX>(r, rmax, g, F);
         const float yv = BACK ? y[rid] : 0.f;
         int t = e >> 2, kin = e & 3;
+        DBG_CHECK(t >= 0 && t < max_steps);
         const int4 nodes = __ldg(tnode + t);
+        DBG_CHECK(nodes.x >= 0 && nodes.x < nverts && nodes.y >= 0 && nodes.y < nverts &&
+                  nodes.z >= 0 && nodes.z < nverts && nodes.w >= 0 && nodes.w < nverts);
         // entry face = face kin in outward order (opposite node kin)
         int id0, id1, id2, lp;
         if (kin == 0)      { id0 = nodes.y; id1 = nodes.z; id2 = nodes.w; lp = 1 | 2 << 2 | 3 << 4; }
@@ -600,6 +614,7 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             const bool d0 = j == 0, d1 = j == 1, d2 = j == 2;
             if (more) {
                 t = lo >> 2;
+                DBG_CHECK(t >= 0 && t < max_steps && (int)(hi >> 8) < nverts);
                 ldg_rec256(rec + 2 * (size_t)t, ta, tb);
                 if (!BACK) mut = __ldg(mu + t);
                 X = __ldg(vtx + (int)(hi >> 8));
@@ -668,7 +683,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
                                                           const float* __restrict__ y,
                                                           double* __restrict__ acc,
                                                           unsigned long long* __restrict__ stats,
-                                                          int tw_log) {
+                                                          int tw_log, int nverts) {
     // warp tile: (1 << tw_log) x (32 >> tw_log) pixels; block = 2 x 2 warp tiles
     const int tw = 1 << tw_log, th = 32 >> tw_log;
     const int tiles_u = (nu + 2 * tw - 1) / (2 * tw);
@@ -706,8 +721,9 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
         if (__syncthreads_and(ok)) ax = 2 * kc + (dkc < 0 ? 1 : 0);
     }
     if (e >= 0) {
-#define WALK(AXV) walk_ray<BACK, AXV>(rec, tnode, vtx, ang, beam, a, u, v, rmax, g, max_steps, e, \
-                                      rid, mu, y, acc, sum, n_cross, n_exact, n_lost, n_stuck)
+#define WALK(AXV) walk_ray<BACK, AXV>(rec, tnode, vtx, ang, beam, a, u, v, rmax, g, max_steps, \
+                                      nverts, e, rid, mu, y, acc, sum, n_cross, n_exact, n_lost, \
+                                      n_stuck)
         switch (ax) {
             case 0: WALK(0); break;
             case 1: WALK(1); break;
@@ -807,6 +823,7 @@ __global__ void __launch_bounds__(128) mt_trace_kernel(const int4* __restrict__ 
         int t = e >> 2, prev = -1;
         int steps = 0;
         while (t >= 0) {
+            DBG_CHECK(t >= 0);
             const int4 nd = __ldg(tnode + t);
             const int ids[4] = {nd.x, nd.y, nd.z, nd.w};
             T P[4][3];
@@ -884,8 +901,10 @@ cudaError_t launch_mt(const DevMesh& m, const LaunchChunk& c, bool back, bool si
 __global__ void gather_mu_kernel(const int* __restrict__ perm, const float* __restrict__ mu,
                                  float* __restrict__ out, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
+         i += (int64_t)gridDim.x * blockDim.x) {
+        DBG_CHECK(perm[i] >= 0 && perm[i] < n);
         out[i] = __ldg(mu + perm[i]);
+    }
 }
 
 __global__ void scatter_x_kernel(const int* __restrict__ perm, const double* __restrict__ acc,
@@ -963,7 +982,7 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
     const int twl = tile_w_log();
     if (m.l2_window_bytes == 0) {
-        trace_kernel<BACK, 4><<<trace_grid_w(c, twl), 128, 0, s>>>(TRACE_ARGS, twl);
+        trace_kernel<BACK, 4><<<trace_grid_w(c, twl), 128, 0, s>>>(TRACE_ARGS, twl, (int)m.nv);
         return;
     }
     // L2 persistence hint for the face-tag records (per launch; the caller's
@@ -981,7 +1000,7 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, trace_kernel<BACK, 4>, TRACE_ARGS, twl);
+    cudaLaunchKernelEx(&cfg, trace_kernel<BACK, 4>, TRACE_ARGS, twl, (int)m.nv);
 }
 
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,

@@ -81,12 +81,13 @@ def lib(build: bool = False) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    path = _build.DEBUG_LIB if os.environ.get("TETPROJ_DEBUG_LIB") == "1" else _build.LIB
     if build:
         _build.build()
-    if not os.path.exists(_build.LIB):
-        raise ImportError(f"{_build.LIB} not built: run `python -m paper_1908_06909_b200._build` "
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -m paper_1908_06909_b200._build` "
                           "or __graft_entry__.build()")
-    L = C.CDLL(_build.LIB)
+    L = C.CDLL(path)
     P = C.c_void_p
     L.tet_mesh_create.argtypes = [P, C.c_int64, P, P, C.c_int64, P, C.c_int64, C.c_int,
                                   C.c_uint32, C.POINTER(C.c_void_p)]

@@ -115,6 +115,22 @@ def test_bvh_entry_finder_identical(case):
     assert sa["crossings"] == sb["crossings"] and sa["rays_hit"] == sb["rays_hit"]
 
 
+def test_debug_build_bounds_checks():
+    """All kernel families on the bounds-checked debug library (device-side
+    traps on any out-of-range index); compute-sanitizer is closed on this pool."""
+    import os
+    import subprocess
+    import sys
+
+    from paper_1908_06909_b200 import _build
+    _build.build_debug()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TETPROJ_DEBUG_LIB="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_case.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "sanitize case ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_empty_detector_misses_mesh():
     m = M.ball_mesh(h=0.3, seed=3)
     geom = G.circular_cone([0.0], 4.0, 8.0, 8, 8, 0.1, 0.1, off_u=200.0)
