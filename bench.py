@@ -209,9 +209,16 @@ def main():
     from paper_1908_06909_b200.dist import dist_backproject
 
     ws, rank, local = dist_env()
+    # one process per GPU over NCCL; TETPROJ_DIST_BACKEND=gloo (testing the
+    # multi-rank logic with several ranks on one GPU) maps ranks onto devices
+    backend = os.environ.get("TETPROJ_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     if ws > 1 and rank != 0:
         dist.barrier()                      # rank 0 builds the mesh cache first
