@@ -284,15 +284,18 @@ def main():
     t_local = sum(ms_step) / 1e3
     crossings_local = (st_f["crossings"] + st_b["crossings"]) * args.steps
     vals = torch.tensor([t_local, sum(ms_f) / 1e3, sum(ms_b) / 1e3, crossings_local,
-                         st_f["crossings"], st_b["crossings"], geom.n_rays], dtype=torch.float64,
-                        device=dev)
+                         st_f["crossings"], st_b["crossings"], geom.n_rays, st_f["rays_hit"],
+                         st_f["lost"] + st_b["lost"], st_f["stuck"] + st_b["stuck"],
+                         st_f["exact_fallbacks"] + st_b["exact_fallbacks"]],
+                        dtype=torch.float64, device=dev)
     if ws > 1:
         mx = vals[:3].clone()
         sm = vals[3:].clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         vals = torch.cat([mx, sm])
-    t_max, tf_max, tb_max, cross_all, cf_all, cb_all, rays_all = vals.tolist()
+    (t_max, tf_max, tb_max, cross_all, cf_all, cb_all, rays_all, hit_all, lost_all, stuck_all,
+     exact_all) = vals.tolist()
 
     # ---- e2e: same metric through the public API with HOST buffers ----
     mu_h = torch.from_numpy(w.mu).pin_memory()
@@ -362,9 +365,8 @@ def main():
             "back": {"crossings_per_s": cb_all * args.steps / tb_max,
                      "mrays_per_s": rays_all * args.steps / tb_max / 1e6,
                      "ms": 1e3 * tb_max / args.steps, "crossings": int(cb_all)},
-            "rays_hit": st_f["rays_hit"], "lost": st_f["lost"] + st_b["lost"],
-            "stuck": st_f["stuck"] + st_b["stuck"],
-            "exact_fallbacks_per_step": st_f["exact_fallbacks"] + st_b["exact_fallbacks"],
+            "rays_hit": int(hit_all), "lost": int(lost_all), "stuck": int(stuck_all),
+            "exact_fallbacks_per_step": int(exact_all),
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
             "mesh_create_s": t_create,
             "roofline": {"bound": "hbm", "kernel": f"trace_kernel<{dom}>",
