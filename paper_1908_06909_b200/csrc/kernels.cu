@@ -416,9 +416,12 @@ __device__ __noinline__ bool exact_entering(const int4* __restrict__ vtx,
 // decides.  Writes entry[ray] = tet<<2 | k and counts conflicts (must be 0).
 __global__ void __launch_bounds__(128, 8) entry_raster_kernel(
     const int4* __restrict__ vtx, const AngleGeom* __restrict__ ang, int beam, int nv, int nu,
-    const EntryItem* __restrict__ items, int* __restrict__ entry,
+    const EntryItem* __restrict__ items, long long n_items, int* __restrict__ entry,
     unsigned long long* __restrict__ stats) {
-    const EntryItem* it = items + blockIdx.x;
+    // one warp per item (4 per block): most hull faces have small footprints
+    const long long item = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (item >= n_items) return;
+    const EntryItem* it = items + item;
     const int npx = it->npx;
     if (npx == 0) return;
     unsigned conflicts = 0, exact = 0;
@@ -426,7 +429,7 @@ __global__ void __launch_bounds__(128, 8) entry_raster_kernel(
     const double c1 = it->c[1], al1 = it->al[1], be1 = it->be[1], b1 = it->bnd[1];
     const double c2 = it->c[2], al2 = it->al[2], be2 = it->be[2], b2 = it->bnd[2];
     const int bw = it->bw, u0 = it->u0, v0 = it->v0, a = it->a, code = it->code;
-    for (int i = threadIdx.x; i < npx; i += blockDim.x) {
+    for (int i = threadIdx.x & 31; i < npx; i += 32) {
         const int dv = i / bw;
         const int u = u0 + (i - dv * bw), v = v0 + dv;
         const double fu = (double)u, fv = (double)v;
@@ -947,8 +950,8 @@ cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry, voi
     const long long n = (long long)m.nb * c.n_angles;
     entry_setup_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
         m.tnode, m.vtx, m.hull, (int)m.nb, c.ang, c.aux, c.beam, c.n_angles, c.nv, c.nu, items);
-    entry_raster_kernel<<<(unsigned)n, 128, 0, s>>>(m.vtx, c.ang, c.beam, c.nv, c.nu, items, entry,
-                                                    stats);
+    entry_raster_kernel<<<(unsigned)((n + 3) / 4), 128, 0, s>>>(m.vtx, c.ang, c.beam, c.nv, c.nu,
+                                                                items, n, entry, stats);
     return cudaGetLastError();
 }
 
