@@ -414,22 +414,18 @@ __device__ __noinline__ bool exact_entering(const int4* __restrict__ vtx,
 // side(c,a) = -1 for the outward-ordered face; the affine value certifies a
 // sign when it clears the item's bound, otherwise the int128 + SoS path
 // decides.  Writes entry[ray] = tet<<2 | k and counts conflicts (must be 0).
-__global__ void __launch_bounds__(128, 8) entry_raster_kernel(
-    const int4* __restrict__ vtx, const AngleGeom* __restrict__ ang, int beam, int nv, int nu,
-    const EntryItem* __restrict__ items, long long n_items, int* __restrict__ entry,
-    unsigned long long* __restrict__ stats) {
-    // one warp per item (4 per block): most hull faces have small footprints
-    const long long item = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
-    if (item >= n_items) return;
-    const EntryItem* it = items + item;
+// Rasterise pixels [first, npx) step `stride` of one item.
+__device__ __forceinline__ void raster_item(const EntryItem* __restrict__ it, int first, int stride,
+                                            const int4* __restrict__ vtx,
+                                            const AngleGeom* __restrict__ ang, int beam, int nv,
+                                            int nu, int* __restrict__ entry, unsigned& conflicts,
+                                            unsigned& exact) {
     const int npx = it->npx;
-    if (npx == 0) return;
-    unsigned conflicts = 0, exact = 0;
     const double c0 = it->c[0], al0 = it->al[0], be0 = it->be[0], b0 = it->bnd[0];
     const double c1 = it->c[1], al1 = it->al[1], be1 = it->be[1], b1 = it->bnd[1];
     const double c2 = it->c[2], al2 = it->al[2], be2 = it->be[2], b2 = it->bnd[2];
     const int bw = it->bw, u0 = it->u0, v0 = it->v0, a = it->a, code = it->code;
-    for (int i = threadIdx.x & 31; i < npx; i += 32) {
+    for (int i = first; i < npx; i += stride) {
         const int dv = i / bw;
         const int u = u0 + (i - dv * bw), v = v0 + dv;
         const double fu = (double)u, fv = (double)v;
@@ -445,6 +441,34 @@ __global__ void __launch_bounds__(128, 8) entry_raster_kernel(
         DBG_CHECK(u >= 0 && u < nu && v >= 0 && v < nv);
         const int old = atomicExch(entry + ((size_t)a * nv + v) * nu + u, code);
         conflicts += (old != -1);
+    }
+}
+
+// Kernel 2: a block takes 4 consecutive (face, angle) items.  Small
+// footprints (<= 512 px, most hull faces) are rasterised by one warp each;
+// large ones by the whole block, so neither many tiny items nor a few big
+// ones leave lanes idle.  The exact entering test: side(a,b) = side(b,c) =
+// side(c,a) = -1 for the outward-ordered face; the affine value certifies a
+// sign when it clears the item's bound, otherwise the int128 + SoS path
+// decides.  Writes entry[ray] = tet<<2 | k and counts conflicts (must be 0).
+__global__ void __launch_bounds__(128, 8) entry_raster_kernel(
+    const int4* __restrict__ vtx, const AngleGeom* __restrict__ ang, int beam, int nv, int nu,
+    const EntryItem* __restrict__ items, long long n_items, int* __restrict__ entry,
+    unsigned long long* __restrict__ stats) {
+    constexpr int kSmall = 512;
+    const long long base = (long long)blockIdx.x * 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned conflicts = 0, exact = 0;
+    if (base + warp < n_items) {
+        const EntryItem* it = items + base + warp;
+        const int npx = it->npx;
+        if (npx > 0 && npx <= kSmall)
+            raster_item(it, lane, 32, vtx, ang, beam, nv, nu, entry, conflicts, exact);
+    }
+    for (int w = 0; w < 4 && base + w < n_items; ++w) {
+        const EntryItem* it = items + base + w;
+        if (it->npx > kSmall)
+            raster_item(it, threadIdx.x, 128, vtx, ang, beam, nv, nu, entry, conflicts, exact);
     }
     if (conflicts) atomicAdd(stats + ST_CONFLICT, (unsigned long long)conflicts);
     if (exact) atomicAdd(stats + ST_EXACT, (unsigned long long)exact);
