@@ -20,6 +20,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace tetproj {
@@ -294,7 +296,7 @@ struct EntryItem {
 __global__ void __launch_bounds__(128) entry_setup_kernel(
     const int4* __restrict__ tnode, const int4* __restrict__ vtx, const int2* __restrict__ hull,
     int nb, const AngleGeom* __restrict__ ang, const AngleAux* __restrict__ aux, int beam,
-    int n_angles, int nv, int nu, EntryItem* __restrict__ items) {
+    int n_angles, int nv, int nu, EntryItem* __restrict__ items, unsigned* __restrict__ n_items) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= nb * n_angles) return;
     const int h = idx % nb, a = idx / nb;
@@ -323,7 +325,6 @@ __global__ void __launch_bounds__(128) entry_setup_kernel(
         const double dd = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
         cull = dn > 1e-9 * dd * nn;
     }
-    items[idx].npx = 0;   // dense item array: culled / empty items stay empty
     if (cull) return;
     // --- detector footprint (bounding box, 1 px margin)
     double umin = 1e300, umax = -1e300, vmin = 1e300, vmax = -1e300;
@@ -393,7 +394,13 @@ __global__ void __launch_bounds__(128) entry_setup_kernel(
     it.npx = (u1 - u0 + 1) * (v1 - v0 + 1);
     it.code = (hk.x << 2) | k;
     it.pad[0] = it.pad[1] = it.pad[2] = 0;
-    items[idx] = it;
+    // compacted item list (order irrelevant: each ray has one entering face)
+    const unsigned mask = __activemask();
+    const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+    unsigned slot = 0;
+    if (lane == leader) slot = atomicAdd(n_items, (unsigned)__popc(mask));
+    slot = __shfl_sync(mask, slot, leader) + __popc(mask & ((1u << lane) - 1));
+    items[slot] = it;
 }
 
 // Rare path of the entry test: all three signs decided by side_direct (fp64
@@ -408,67 +415,101 @@ __device__ __noinline__ bool exact_entering(const int4* __restrict__ vtx,
            side_direct(C, A, r, exact) == -1;
 }
 
-// Kernel 2 (one block per (face, angle) item; empty items exit at once, the
-// block scheduler balances the uneven footprints): the exact entering test for
-// every pixel of the item's box -- entering iff side(a,b) = side(b,c) =
-// side(c,a) = -1 for the outward-ordered face; the affine value certifies a
-// sign when it clears the item's bound, otherwise the int128 + SoS path
-// decides.  Writes entry[ray] = tet<<2 | k and counts conflicts (must be 0).
-// Rasterise pixels [first, npx) step `stride` of one item.
-__device__ __forceinline__ void raster_item(const EntryItem* __restrict__ it, int first, int stride,
-                                            const int4* __restrict__ vtx,
-                                            const AngleGeom* __restrict__ ang, int beam, int nv,
-                                            int nu, int* __restrict__ entry, unsigned& conflicts,
-                                            unsigned& exact) {
-    const int npx = it->npx;
-    const double c0 = it->c[0], al0 = it->al[0], be0 = it->be[0], b0 = it->bnd[0];
-    const double c1 = it->c[1], al1 = it->al[1], be1 = it->be[1], b1 = it->bnd[1];
-    const double c2 = it->c[2], al2 = it->al[2], be2 = it->be[2], b2 = it->bnd[2];
-    const int bw = it->bw, u0 = it->u0, v0 = it->v0, a = it->a, code = it->code;
-    for (int i = first; i < npx; i += stride) {
-        const int dv = i / bw;
-        const int u = u0 + (i - dv * bw), v = v0 + dv;
-        const double fu = (double)u, fv = (double)v;
-        const double sab = fma(fv, be0, fma(fu, al0, c0));
-        if (sab > b0) continue;
-        const double sbc = fma(fv, be1, fma(fu, al1, c1));
-        if (sbc > b1) continue;
-        const double sca = fma(fv, be2, fma(fu, al2, c2));
-        if (sca > b2) continue;
-        if (sab >= -b0 || sbc >= -b1 || sca >= -b2) {   // a sign the bound cannot certify
-            if (!exact_entering(vtx, ang, beam, a, u, v, it->ia, it->ib, it->ic, exact)) continue;
-        }
-        DBG_CHECK(u >= 0 && u < nu && v >= 0 && v < nv);
-        const int old = atomicExch(entry + ((size_t)a * nv + v) * nu + u, code);
-        conflicts += (old != -1);
+// Conservative u-range of one row for one edge.  A pixel survives the
+// per-pixel test only if the computed side f = c + u al + v be is <= bnd;
+// the evaluation error is below bnd, so the exact value is <= 2 bnd, i.e.
+// u al <= r := 2 bnd - c - v be.  r and r/al are rounded, so the range is
+// widened by 1 px + the rounding error of r in pixels; a nearly u-parallel
+// edge (error not below 2^20 px) does not narrow the row.  Widening only
+// costs tests: every pixel inside is still tested exactly.
+__device__ __forceinline__ void clip_row(double c, double al, double be, double bnd, double fv,
+                                         int& lo, int& hi) {
+    const double vb = fv * be;
+    const double r = 2.0 * bnd - c - vb;
+    const double aal = fabs(al);
+    const double margin = 1.0 + 0x1p-50 * (2.0 * bnd + fabs(c) + fabs(vb)) / aal;
+    if (!(margin < 0x1p20)) return;            // al == 0 or too ill-conditioned
+    const double x = r / al;
+    if (!(fabs(x) < 0x1p30)) {                 // far outside the detector
+        if ((al > 0) == (x < 0)) { lo = 1; hi = 0; }
+        return;
     }
+    if (al > 0) hi = min(hi, (int)floor(x + margin));
+    else        lo = max(lo, (int)ceil(x - margin));
 }
 
-// Kernel 2: a block takes 4 consecutive (face, angle) items.  Small
-// footprints (<= 512 px, most hull faces) are rasterised by one warp each;
-// large ones by the whole block, so neither many tiny items nor a few big
-// ones leave lanes idle.  The exact entering test: side(a,b) = side(b,c) =
-// side(c,a) = -1 for the outward-ordered face; the affine value certifies a
-// sign when it clears the item's bound, otherwise the int128 + SoS path
-// decides.  Writes entry[ray] = tet<<2 | k and counts conflicts (must be 0).
+// Kernel 2 (persistent grid, one warp per (face, angle) item): scanline
+// rasterisation of the face's footprint box.  32 rows at a time, lane r
+// clips row r against the three edge half-planes (conservatively), a warp
+// scan packs the surviving pixels, and the lanes test them densely -- an
+// entering test is side(a,b) = side(b,c) = side(c,a) = -1 for the
+// outward-ordered face; the affine value certifies a sign when it clears
+// the item's bound, otherwise the int128 + SoS path decides.  Writes
+// entry[ray] = tet<<2 | k and counts conflicts (must be 0).
 __global__ void __launch_bounds__(128, 8) entry_raster_kernel(
     const int4* __restrict__ vtx, const AngleGeom* __restrict__ ang, int beam, int nv, int nu,
-    const EntryItem* __restrict__ items, long long n_items, int* __restrict__ entry,
-    unsigned long long* __restrict__ stats) {
-    constexpr int kSmall = 512;
-    const long long base = (long long)blockIdx.x * 4;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const EntryItem* __restrict__ items, const unsigned* __restrict__ n_items_p,
+    unsigned* __restrict__ queue, int* __restrict__ entry, unsigned long long* __restrict__ stats) {
+    const unsigned n_items = n_items_p[0];
+    const int lane = threadIdx.x & 31;
     unsigned conflicts = 0, exact = 0;
-    if (base + warp < n_items) {
-        const EntryItem* it = items + base + warp;
+    for (;;) {   // dynamic queue: footprints vary by orders of magnitude
+        unsigned item = 0;
+        if (lane == 0) item = atomicAdd(queue, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= n_items) break;
+        const EntryItem* it = items + item;
         const int npx = it->npx;
-        if (npx > 0 && npx <= kSmall)
-            raster_item(it, lane, 32, vtx, ang, beam, nv, nu, entry, conflicts, exact);
-    }
-    for (int w = 0; w < 4 && base + w < n_items; ++w) {
-        const EntryItem* it = items + base + w;
-        if (it->npx > kSmall)
-            raster_item(it, threadIdx.x, 128, vtx, ang, beam, nv, nu, entry, conflicts, exact);
+        const double c0 = it->c[0], al0 = it->al[0], be0 = it->be[0], b0 = it->bnd[0];
+        const double c1 = it->c[1], al1 = it->al[1], be1 = it->be[1], b1 = it->bnd[1];
+        const double c2 = it->c[2], al2 = it->al[2], be2 = it->be[2], b2 = it->bnd[2];
+        const int bw = it->bw, u0 = it->u0, v0 = it->v0, a = it->a, code = it->code;
+        const int nrows = npx / bw;
+        for (int r0 = 0; r0 < nrows; r0 += 32) {
+            int lo = u0, hi = u0 + bw - 1;
+            if (r0 + lane < nrows) {
+                const double fv = (double)(v0 + r0 + lane);
+                clip_row(c0, al0, be0, b0, fv, lo, hi);
+                clip_row(c1, al1, be1, b1, fv, lo, hi);
+                clip_row(c2, al2, be2, b2, fv, lo, hi);
+            } else {
+                hi = lo - 1;
+            }
+            const int len = max(0, hi - lo + 1);
+            int inc = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            const int total = __shfl_sync(0xffffffffu, inc, 31);
+            const int exc = inc - len;
+            for (int base = 0; base < total; base += 32) {
+                const int i = base + lane;
+                int j = 0;   // row of pixel i: number of rows whose inclusive end is <= i
+#pragma unroll
+                for (int st = 16; st; st >>= 1)
+                    if (__shfl_sync(0xffffffffu, inc, j + st - 1) <= i) j += st;
+                const int ej = __shfl_sync(0xffffffffu, exc, j);
+                const int lj = __shfl_sync(0xffffffffu, lo, j);
+                if (i >= total) continue;
+                const int u = lj + (i - ej), v = v0 + r0 + j;
+                const double fu = (double)u, fv = (double)v;
+                const double sab = fma(fv, be0, fma(fu, al0, c0));
+                if (sab > b0) continue;
+                const double sbc = fma(fv, be1, fma(fu, al1, c1));
+                if (sbc > b1) continue;
+                const double sca = fma(fv, be2, fma(fu, al2, c2));
+                if (sca > b2) continue;
+                if (sab >= -b0 || sbc >= -b1 || sca >= -b2) {   // a sign the bound cannot certify
+                    if (!exact_entering(vtx, ang, beam, a, u, v, it->ia, it->ib, it->ic, exact))
+                        continue;
+                }
+                DBG_CHECK(u >= u0 && u < u0 + bw && u < nu && v >= 0 && v < nv);
+                const int old = atomicExch(entry + ((size_t)a * nv + v) * nu + u, code);
+                conflicts += (old != -1);
+            }
+        }
     }
     if (conflicts) atomicAdd(stats + ST_CONFLICT, (unsigned long long)conflicts);
     if (exact) atomicAdd(stats + ST_EXACT, (unsigned long long)exact);
@@ -970,12 +1011,24 @@ cudaError_t launch_entry_bvh(const DevMesh& m, const LaunchChunk& c, int* entry,
 
 cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry, void* scratch,
                          unsigned long long* stats, cudaStream_t s) {
+    unsigned* n_items = (unsigned*)scratch;
     EntryItem* items = (EntryItem*)((char*)scratch + 256);
     const long long n = (long long)m.nb * c.n_angles;
+    cudaError_t e = cudaMemsetAsync(n_items, 0, 2 * sizeof(unsigned), s);   // count, queue
+    if (e != cudaSuccess) return e;
     entry_setup_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
-        m.tnode, m.vtx, m.hull, (int)m.nb, c.ang, c.aux, c.beam, c.n_angles, c.nv, c.nu, items);
-    entry_raster_kernel<<<(unsigned)((n + 3) / 4), 128, 0, s>>>(m.vtx, c.ang, c.beam, c.nv, c.nu,
-                                                                items, n, entry, stats);
+        m.tnode, m.vtx, m.hull, (int)m.nb, c.ang, c.aux, c.beam, c.n_angles, c.nv, c.nu, items,
+        n_items);
+    static const unsigned grid = [] {
+        int dev = 0, sms = 148, per = 8;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, entry_raster_kernel, 128, 0);
+        return (unsigned)(sms * (per > 0 ? per : 1));
+    }();
+    const unsigned blocks = (unsigned)std::min<long long>(grid, (n + 3) / 4);
+    entry_raster_kernel<<<blocks, 128, 0, s>>>(m.vtx, c.ang, c.beam, c.nv, c.nu, items, n_items,
+                                               n_items + 1, entry, stats);
     return cudaGetLastError();
 }
 
