@@ -105,12 +105,18 @@ __device__ __noinline__ int exact_side_ids(const int4* __restrict__ vtx,
 // within ~26 eps Amax^2 of det/D_k (Amax >= |X - o| for every vertex), far
 // below tau = 2^-40 Amax^2.  z' of the crossing
 // points gives the chord: |D|/D_k * dz' * g.
+// Shear frame of one ray (dominant axis k, sigma = sign D_k):
+//   z' = sigma X_k (absolute: chords only use differences), so z' grows along the ray
+//   x' = (X_k1 - c1) - sx z',  sx = D_k1/|D_k|,  c1 = o_k1 - sx sigma o_k   (y' alike)
+// i.e. x' = A_k1 - (D_k1/D_k) A_k with A = X - o: the ray is the z' axis and
+// det[a-o, b-o, p-o] = D_k (x'_a y'_b - y'_a x'_b).  Error bound and tau: DESIGN.md §5.
 struct Frame {
-    double sx, sy;         // D_k1/D_k, D_k2/D_k
-    double o1, o2, o3;     // o_k1, o_k2, o_k
+    double sx, sy;         // D_k1/|D_k|, D_k2/|D_k|
+    double c1, c2;         // o_k1 - sx sigma o_k, o_k2 - sy sigma o_k
     double tau;            // sign-filter threshold
-    double scale;          // |D|/D_k * g (signed: z' decreases along the ray if D_k < 0)
+    double scale;          // |D|/|D_k| * g  (> 0)
     int k1, k2, k3;        // coordinate permutation
+    int neg;               // sigma < 0
 };
 
 __device__ __forceinline__ double comp(long long x, long long y, long long z, int k) {
@@ -128,16 +134,18 @@ __device__ __forceinline__ void make_frame(const RayPts& r, double rmax, double 
     const double dk = comp(Dx, Dy, Dz, k);
     if (dk < 0) { const int tmp = k1; k1 = k2; k2 = tmp; }
     F.k1 = k1; F.k2 = k2; F.k3 = k;
-    F.sx = comp(Dx, Dy, Dz, k1) / dk;
-    F.sy = comp(Dx, Dy, Dz, k2) / dk;
-    F.o1 = comp(r.ox, r.oy, r.oz, k1);
-    F.o2 = comp(r.ox, r.oy, r.oz, k2);
-    F.o3 = comp(r.ox, r.oy, r.oz, k);
+    F.neg = dk < 0;
+    const double adk = fabs(dk);
+    F.sx = comp(Dx, Dy, Dz, k1) / adk;
+    F.sy = comp(Dx, Dy, Dz, k2) / adk;
+    const double so3 = F.neg ? -comp(r.ox, r.oy, r.oz, k) : comp(r.ox, r.oy, r.oz, k);
+    F.c1 = fma(-F.sx, so3, comp(r.ox, r.oy, r.oz, k1));
+    F.c2 = fma(-F.sy, so3, comp(r.ox, r.oy, r.oz, k2));
     const double ox = (double)r.ox, oy = (double)r.oy, oz = (double)r.oz;
     const double amax = sqrt(ox * ox + oy * oy + oz * oz) + rmax;
     F.tau = amax * amax * 0x1p-40;
     const double dx = (double)Dx, dy = (double)Dy, dz = (double)Dz;
-    F.scale = sqrt(dx * dx + dy * dy + dz * dz) / dk * g;
+    F.scale = sqrt(dx * dx + dy * dy + dz * dz) / adk * g;
 }
 
 // Branch-free selects (the ternary chains compiled to divergent branches).
@@ -161,11 +169,10 @@ __device__ __forceinline__ double rcp_nr(double x) {
 
 __device__ __forceinline__ void xform(const Frame& F, const int4 v, double& x, double& y,
                                       double& z) {
-    const double a1 = (double)icomp(v, F.k1) - F.o1;   // exact (|.| < 2^33)
-    const double a2 = (double)icomp(v, F.k2) - F.o2;
-    z = (double)icomp(v, F.k3) - F.o3;
-    x = fma(-F.sx, z, a1);
-    y = fma(-F.sy, z, a2);
+    const int zk = icomp(v, F.k3);
+    z = (double)(F.neg ? -zk : zk);
+    x = fma(-F.sx, z, (double)icomp(v, F.k1) - F.c1);
+    y = fma(-F.sy, z, (double)icomp(v, F.k2) - F.c2);
 }
 
 // Compile-time axis variants of the shear frame: AX = 2*k + swap (k = shear
@@ -201,18 +208,21 @@ __device__ __forceinline__ void make_frame_ax(const RayPts& r, double rmax, doub
     } else {
         using A = Axis<AX>;
         const long long Dx = r.px - r.ox, Dy = r.py - r.oy, Dz = r.pz - r.oz;
-        const double dk = (double)pick<A::k>(Dx, Dy, Dz);
-        F.sx = (double)pick<A::K1>(Dx, Dy, Dz) / dk;
-        F.sy = (double)pick<A::K2>(Dx, Dy, Dz) / dk;
-        F.o1 = (double)pick<A::K1>(r.ox, r.oy, r.oz);
-        F.o2 = (double)pick<A::K2>(r.ox, r.oy, r.oz);
-        F.o3 = (double)pick<A::k>(r.ox, r.oy, r.oz);
+        // AX & 1 <=> D_k < 0 (the block vote guarantees the sign)
+        const double adk = fabs((double)pick<A::k>(Dx, Dy, Dz));
+        F.sx = (double)pick<A::K1>(Dx, Dy, Dz) / adk;
+        F.sy = (double)pick<A::K2>(Dx, Dy, Dz) / adk;
+        const double o3 = (double)pick<A::k>(r.ox, r.oy, r.oz);
+        const double so3 = (AX & 1) ? -o3 : o3;
+        F.c1 = fma(-F.sx, so3, (double)pick<A::K1>(r.ox, r.oy, r.oz));
+        F.c2 = fma(-F.sy, so3, (double)pick<A::K2>(r.ox, r.oy, r.oz));
+        F.neg = AX & 1;
         const double ox = (double)r.ox, oy = (double)r.oy, oz = (double)r.oz;
         const double amax = (sqrt(ox * ox + oy * oy + oz * oz) + rmax) *
                             (1.0 + fabs(F.sx) + fabs(F.sy)) * 0.5;
         F.tau = amax * amax * 0x1p-38;
         const double dx = (double)Dx, dy = (double)Dy, dz = (double)Dz;
-        F.scale = sqrt(dx * dx + dy * dy + dz * dz) / dk * g;
+        F.scale = sqrt(dx * dx + dy * dy + dz * dz) / adk * g;
         F.k1 = A::K1; F.k2 = A::K2; F.k3 = A::k;
     }
 }
@@ -224,11 +234,10 @@ __device__ __forceinline__ void xform_ax(const Frame& F, const int4 v, double& x
         xform(F, v, x, y, z);
     } else {
         using A = Axis<AX>;
-        const double a1 = (double)pick4<A::K1>(v) - F.o1;   // exact (|.| < 2^33)
-        const double a2 = (double)pick4<A::K2>(v) - F.o2;
-        z = (double)pick4<A::k>(v) - F.o3;
-        x = fma(-F.sx, z, a1);
-        y = fma(-F.sy, z, a2);
+        const double zz = (double)pick4<A::k>(v);
+        z = (AX & 1) ? -zz : zz;
+        x = fma(-F.sx, z, (double)pick4<A::K1>(v) - F.c1);
+        y = fma(-F.sy, z, (double)pick4<A::K2>(v) - F.c2);
     }
 }
 
@@ -586,6 +595,22 @@ __global__ void __launch_bounds__(128) entry_bvh_kernel(const int4* __restrict__
 }
 
 // ------------------------------------------------------------ walker ----
+// j (dropped slot) per sign code neg = n0 | n1<<1 | n2<<2, 2 bits each; 3 = lost
+constexpr unsigned kExitLUT = 3u | 2u << 2 | 0u << 4 | 0u << 6 | 1u << 8 | 2u << 10 | 1u << 12 |
+                              3u << 14;
+
+// [|a| <= t or |b| <= t or |c| <= t] as one predicate chain (keeps nvcc from
+// rewriting it as an fp64 min with NaN fix-ups)
+__device__ __forceinline__ bool any_abs_le(double a, double b, double c, double t) {
+    unsigned r;
+    asm("{\n\t.reg .pred q;\n\t.reg .f64 x, y, z;\n\t"
+        "abs.f64 x, %1;\n\tabs.f64 y, %2;\n\tabs.f64 z, %3;\n\t"
+        "setp.le.f64 q, x, %4;\n\tsetp.le.or.f64 q, y, %4, q;\n\t"
+        "setp.le.or.f64 q, z, %4, q;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+        : "=r"(r) : "d"(a), "d"(b), "d"(c), "d"(t));
+    return r != 0;
+}
+
 // Certified sign of a side value (filter, else exact int128 + SoS).
 #define SIGN_OF(val, id_other, out)                                                   \
     do {                                                                            \
@@ -614,18 +639,21 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
         const RayPts r = ray_points(ang[a], beam, u, v);
         Frame F;
         make_frame_ax<AX>(r, rmax, g, F);
-        const float yv = BACK ? y[rid] : 0.f;
-        int t = e >> 2, kin = e & 3;
+        // chord = (z'_out - z'_in) * scale; scale is folded into y (back) or
+        // applied once to the ray sum (forward)
+        const double wy = BACK ? (double)y[rid] * F.scale : 0.0;
+        const int t0 = e >> 2, kin = e & 3;
+        int t = t0;
         DBG_CHECK(t >= 0 && t < max_steps);
         const int4 nodes = __ldg(tnode + t);
         DBG_CHECK(nodes.x >= 0 && nodes.x < nverts && nodes.y >= 0 && nodes.y < nverts &&
                   nodes.z >= 0 && nodes.z < nverts && nodes.w >= 0 && nodes.w < nverts);
         // entry face = face kin in outward order (opposite node kin)
-        int id0, id1, id2, lp;
-        if (kin == 0)      { id0 = nodes.y; id1 = nodes.z; id2 = nodes.w; lp = 1 | 2 << 2 | 3 << 4; }
-        else if (kin == 1) { id0 = nodes.x; id1 = nodes.w; id2 = nodes.z; lp = 0 | 3 << 2 | 2 << 4; }
-        else if (kin == 2) { id0 = nodes.x; id1 = nodes.y; id2 = nodes.w; lp = 0 | 1 << 2 | 3 << 4; }
-        else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; lp = 0 | 2 << 2 | 1 << 4; }
+        int id0, id1, id2;
+        if (kin == 0)      { id0 = nodes.y; id1 = nodes.z; id2 = nodes.w; }
+        else if (kin == 1) { id0 = nodes.x; id1 = nodes.w; id2 = nodes.z; }
+        else if (kin == 2) { id0 = nodes.x; id1 = nodes.y; id2 = nodes.w; }
+        else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; }
         int iap = sel4(nodes, kin);
         double x0, y0, z0, x1, y1, z1, x2, y2, z2;
         xform_ax<AX>(F, __ldg(vtx + id0), x0, y0, z0);
@@ -645,6 +673,7 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
         // run while they are in flight.
         int4 ta, tb;
         ldg_rec256(rec + 2 * (size_t)t, ta, tb);             // face tags of t (32 B)
+        int4 nd = nodes;                                     // node ids of t (16 B)
         float mut = 0.f;
         if (!BACK) mut = __ldg(mu + t);
         int4 X = __ldg(vtx + iap);                          // apex vertex (16 B)
@@ -660,23 +689,32 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             // filter cannot certify is decided exactly (rare branch).  With
             // n_k = [sign p_k = -1]: i = 0 for (1,0,*), 1 for (*,1,0), 2 for
             // (0,*,1); (0,0,0) and (1,1,1) cannot occur for an entering ray.
-            bool n0 = p0 < -F.tau, n1 = p1 < -F.tau, n2 = p2 < -F.tau;
-            const bool u0 = !n0 && !(p0 > F.tau), u1 = !n1 && !(p1 > F.tau),
-                       u2 = !n2 && !(p2 > F.tau);
-            if (u0 | u1 | u2) {
-                if (u0) { n0 = exact_side_ids(vtx, ang, beam, a, u, v, iap, id0) < 0; ++n_exact; }
-                if (u1) { n1 = exact_side_ids(vtx, ang, beam, a, u, v, iap, id1) < 0; ++n_exact; }
-                if (u2) { n2 = exact_side_ids(vtx, ang, beam, a, u, v, iap, id2) < 0; ++n_exact; }
+            // certified iff |p| > tau; then the sign bit is the sign.  neg =
+            // (n0, n1, n2) with n_k = [sign p_k = -1] as bits 0..2.
+            unsigned neg = ((unsigned)__double2hiint(p0) >> 31) |
+                           (((unsigned)__double2hiint(p1) >> 30) & 2u) |
+                           (((unsigned)__double2hiint(p2) >> 29) & 4u);
+            if (any_abs_le(p0, p1, p2, F.tau)) {
+                const unsigned m = neg;
+                neg = 0;
+                neg |= fabs(p0) <= F.tau ? (exact_side_ids(vtx, ang, beam, a, u, v, iap, id0) < 0 ? 1u : 0u) : (m & 1u);
+                neg |= fabs(p1) <= F.tau ? (exact_side_ids(vtx, ang, beam, a, u, v, iap, id1) < 0 ? 2u : 0u) : (m & 2u);
+                neg |= fabs(p2) <= F.tau ? (exact_side_ids(vtx, ang, beam, a, u, v, iap, id2) < 0 ? 4u : 0u) : (m & 4u);
+                n_exact += (fabs(p0) <= F.tau) + (fabs(p1) <= F.tau) + (fabs(p2) <= F.tau);
             }
-            const bool c0 = n0 && !n1;            // p0 = -1, p1 = +1
-            const bool c1 = n1 && !n2 && !c0;     // p1 = -1, p2 = +1
-            n_lost += (n0 == n1 && n1 == n2) ? 1u : 0u;
+            // exit face (apex, slot i, slot i+1) for the unique i with n_i = 1,
+            // n_{i+1} = 0; it drops slot j = i+2.  j by table on neg:
+            // 1,5 -> i=0, j=2;  2,3 -> i=1, j=0;  4,6 -> i=2, j=1;  0,7 -> lost (3)
+            const int j = (int)((kExitLUT >> (2 * neg)) & 3u);
+            const bool c0 = j == 2, c1 = j == 0;
+            n_lost += j == 3 ? 1u : 0u;
             // exit through the face opposite slot j = i+2 (local index L in t)
-            const int j = selp(2, selp(0, 1, c1), c0);
-            const int L = (lp >> (2 * j)) & 3;
+            // local index in t of the dropped slot's vertex, from t's node list
+            const int idj = selp(id0, selp(id1, id2, j == 1), j == 0);
+            const int L = selp(0, selp(1, selp(2, 3, idj == nd.z), idj == nd.y), idj == nd.x);
             const int lo = selp(selp(ta.x, ta.z, L == 0), selp(tb.x, tb.z, L == 2), L < 2);
             const unsigned hi = (unsigned)selp(selp(ta.y, ta.w, L == 0), selp(tb.y, tb.w, L == 2), L < 2);
-            const bool more = lo >= 0 && --steps_left != 0;
+            const bool more = lo >= 0 && j != 3 && --steps_left != 0;
             const int tcur = t;
             const float mcur = mut;
             const bool d0 = j == 0, d1 = j == 1, d2 = j == 2;
@@ -684,16 +722,9 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
                 t = lo >> 2;
                 DBG_CHECK(t >= 0 && t < max_steps && (int)(hi >> 8) < nverts);
                 ldg_rec256(rec + 2 * (size_t)t, ta, tb);
+                nd = __ldg(tnode + t);
                 if (!BACK) mut = __ldg(mu + t);
                 X = __ldg(vtx + (int)(hi >> 8));
-                // local indices in the next tet: kept slots map through `map`,
-                // the dropped slot j receives the current apex (local index kin)
-                const int s0 = selp(kin, lp & 3, d0);
-                const int s1 = selp(kin, (lp >> 2) & 3, d1);
-                const int s2 = selp(kin, (lp >> 4) & 3, d2);
-                lp = ((hi >> (2 * s0)) & 3) | (((hi >> (2 * s1)) & 3) << 2) |
-                     (((hi >> (2 * s2)) & 3) << 4);
-                kin = lo & 3;
             }
             // ---- chord of step k (overlaps the gathers of step k+1)
             // crossing point weights: apex |s(i,i+1)|, slot i |p_{i+1}|, slot i+1 |p_i|.
@@ -715,17 +746,17 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
                 zout = zin;
                 ++n_exact;
             }
-            // (zout - zin) * scale >= 0 up to rounding; an exact zero-length
-            // crossing may come out as -1e-16 R, which is harmless in the sum
-            const double chord = (zout - zin) * F.scale;
+            // zout - zin >= 0 up to rounding; an exact zero-length crossing
+            // may come out as -1e-16 R, which is harmless in the sum
+            const double dz = zout - zin;
             if (BACK) {
-                if (chord > 0.0) atomicAdd(acc + tcur, chord * (double)yv);
+                if (dz > 0.0) atomicAdd(acc + tcur, dz * wy);
             } else {
-                sum = fma(chord, (double)mcur, sum);
+                sum = fma(dz, (double)mcur, sum);
             }
             ++n_cross;
             if (!more) {
-                if (lo >= 0) ++n_stuck;
+                if (lo >= 0 && j != 3) ++n_stuck;
                 break;
             }
             // the apex takes the dropped slot i+2 (cyclic order is preserved);
@@ -736,6 +767,7 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             zin = zout;
             iap = (int)(hi >> 8);
         }
+        if (!BACK) sum *= F.scale;
     }
 
 template <bool BACK, int MINB>

@@ -82,6 +82,9 @@ def lib(build: bool = False) -> C.CDLL:
     if _lib is not None:
         return _lib
     path = _build.DEBUG_LIB if os.environ.get("TETPROJ_DEBUG_LIB") == "1" else _build.LIB
+    variant = os.environ.get("TETPROJ_LIB_VARIANT")   # A/B measurements (experiments/)
+    if variant:
+        path = os.path.join(os.path.dirname(_build.LIB), "variants", f"libtetproj_{variant}.so")
     if build:
         _build.build()
     if not os.path.exists(path):
