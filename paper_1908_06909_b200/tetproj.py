@@ -85,8 +85,8 @@ def lib(build: bool = False) -> C.CDLL:
     variant = os.environ.get("TETPROJ_LIB_VARIANT")   # A/B measurements (experiments/)
     if variant:
         path = os.path.join(os.path.dirname(_build.LIB), "variants", f"libtetproj_{variant}.so")
-    if build:
-        _build.build()
+    if build or (not variant and os.environ.get("TETPROJ_DEBUG_LIB") != "1" and _build.stale()):
+        _build.build()   # never load a library older than its sources
     if not os.path.exists(path):
         raise ImportError(f"{path} not built: run `python -m paper_1908_06909_b200._build` "
                           "or __graft_entry__.build()")
