@@ -716,14 +716,12 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             const unsigned hi = (unsigned)selp(selp(ta.y, ta.w, L == 0), selp(tb.y, tb.w, L == 2), L < 2);
             const bool more = lo >= 0 && j != 3 && --steps_left != 0;
             const int tcur = t;
-            const float mcur = mut;
             const bool d0 = j == 0, d1 = j == 1, d2 = j == 2;
             if (more) {
                 t = lo >> 2;
                 DBG_CHECK(t >= 0 && t < max_steps && (int)(hi >> 8) < nverts);
                 ldg_rec256(rec + 2 * (size_t)t, ta, tb);
                 nd = __ldg(tnode + t);
-                if (!BACK) mut = __ldg(mu + t);
                 X = __ldg(vtx + (int)(hi >> 8));
             }
             // ---- chord of step k (overlaps the gathers of step k+1)
@@ -752,13 +750,17 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             if (BACK) {
                 if (dz > 0.0) atomicAdd(acc + tcur, dz * wy);
             } else {
-                sum = fma(dz, (double)mcur, sum);
+                sum = fma(dz, (double)mut, sum);
             }
             ++n_cross;
             if (!more) {
                 if (lo >= 0 && j != 3) ++n_stuck;
                 break;
             }
+            // mu of the next tet: issued after this step's use so no second
+            // register (and no copy that waits on the load) is needed; it is
+            // consumed at the end of the next step
+            if (!BACK) mut = __ldg(mu + t);
             // the apex takes the dropped slot i+2 (cyclic order is preserved);
             // s_{i+1} <- -p_{i+1}, s_{i+2} <- p_i
             if (d0) { x0 = x3; y0 = y3; z0 = z3; id0 = iap; s20 = -p2; s01 = p1; }
