@@ -95,6 +95,27 @@ __device__ __noinline__ int exact_side_ids(const int4* __restrict__ vtx,
     return sos_side(A.x, A.y, A.z, B.x, B.y, B.z, r.ox, r.oy, r.oz, r.px, r.py, r.pz);
 }
 
+// The walker's rare exact path: the thread's own ray is recomputed from its
+// grid position (same mapping as trace_kernel), so (a, u, v) need not stay
+// live in registers across the walk loop.
+__device__ __forceinline__ void thread_pixel(int nu, int tw_log, int& a, int& u, int& v) {
+    const int tw = 1 << tw_log, th = 32 >> tw_log;
+    const int tiles_u = (nu + 2 * tw - 1) / (2 * tw);
+    const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    a = blockIdx.y;
+    u = bx * 2 * tw + (w & 1) * tw + (lane & (tw - 1));
+    v = by * 2 * th + (w >> 1) * th + (lane >> tw_log);
+}
+
+__device__ __noinline__ int exact_side_here(const int4* __restrict__ vtx,
+                                            const AngleGeom* __restrict__ ang, int beam, int nu,
+                                            int tw_log, int ia, int ib) {
+    int a, u, v;
+    thread_pixel(nu, tw_log, a, u, v);
+    return exact_side_ids(vtx, ang, beam, a, u, v, ia, ib);
+}
+
 // ------------------------------------------------------------ frame -----
 // Shear frame of a ray (the projection along the ray onto the coordinate
 // plane orthogonal to its dominant axis k):
@@ -611,12 +632,6 @@ __device__ __forceinline__ bool any_abs_le(double a, double b, double c, double 
     return r != 0;
 }
 
-// Certified sign of a side value (filter, else exact int128 + SoS).
-#define SIGN_OF(val, id_other, out)                                                   \
-    do {                                                                            \
-        out = (val) > F.tau ? 1 : ((val) < -F.tau ? -1 : 0);                        \
-        if (!out) { out = exact_side_ids(vtx, ang, beam, a, u, v, iap, id_other); ++n_exact; } \
-    } while (0)
 
 // One thread per ray, 8x4-pixel warp tiles (16x8 per block).
 // State: the entry face in three fixed slots k = 0,1,2 in cyclic order (shear
@@ -630,8 +645,8 @@ template <bool BACK, int AX>
 __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int4* __restrict__ tnode,
                                          const int4* __restrict__ vtx,
                                          const AngleGeom* __restrict__ ang, int beam, int a, int u,
-                                         int v, double rmax, double g, int max_steps,
-                                         int nverts, int e, size_t rid,
+                                         int v, int nu, int tw_log, double rmax, double g,
+                                         int max_steps, int nverts, int e, size_t rid,
                                          const float* __restrict__ mu,
                                          const float* __restrict__ y, double* __restrict__ acc,
                                          double& sum, unsigned& n_cross, unsigned& n_exact,
@@ -666,7 +681,7 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             const double sw = w0 + w1 + w2;
             zin = sw > 0 ? (w0 * z0 + w1 * z1 + w2 * z2) / sw : (z0 + z1 + z2) * (1.0 / 3.0);
         }
-        int steps_left = max_steps;
+        int steps = 0;   // crossings done before this one
         // Software-pipelined by one step: the gathers of step k+1 (face tags of
         // the next tet, its apex vertex, mu) are issued as soon as step k's
         // exit face is known, and step k's chord / accumulation / slot update
@@ -697,9 +712,9 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             if (any_abs_le(p0, p1, p2, F.tau)) {
                 const unsigned m = neg;
                 neg = 0;
-                neg |= fabs(p0) <= F.tau ? (exact_side_ids(vtx, ang, beam, a, u, v, iap, id0) < 0 ? 1u : 0u) : (m & 1u);
-                neg |= fabs(p1) <= F.tau ? (exact_side_ids(vtx, ang, beam, a, u, v, iap, id1) < 0 ? 2u : 0u) : (m & 2u);
-                neg |= fabs(p2) <= F.tau ? (exact_side_ids(vtx, ang, beam, a, u, v, iap, id2) < 0 ? 4u : 0u) : (m & 4u);
+                neg |= fabs(p0) <= F.tau ? (exact_side_here(vtx, ang, beam, nu, tw_log, iap, id0) < 0 ? 1u : 0u) : (m & 1u);
+                neg |= fabs(p1) <= F.tau ? (exact_side_here(vtx, ang, beam, nu, tw_log, iap, id1) < 0 ? 2u : 0u) : (m & 2u);
+                neg |= fabs(p2) <= F.tau ? (exact_side_here(vtx, ang, beam, nu, tw_log, iap, id2) < 0 ? 4u : 0u) : (m & 4u);
                 n_exact += (fabs(p0) <= F.tau) + (fabs(p1) <= F.tau) + (fabs(p2) <= F.tau);
             }
             // exit face (apex, slot i, slot i+1) for the unique i with n_i = 1,
@@ -707,14 +722,13 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             // 1,5 -> i=0, j=2;  2,3 -> i=1, j=0;  4,6 -> i=2, j=1;  0,7 -> lost (3)
             const int j = (int)((kExitLUT >> (2 * neg)) & 3u);
             const bool c0 = j == 2, c1 = j == 0;
-            n_lost += j == 3 ? 1u : 0u;
             // exit through the face opposite slot j = i+2 (local index L in t)
             // local index in t of the dropped slot's vertex, from t's node list
             const int idj = selp(id0, selp(id1, id2, j == 1), j == 0);
             const int L = selp(0, selp(1, selp(2, 3, idj == nd.z), idj == nd.y), idj == nd.x);
             const int lo = selp(selp(ta.x, ta.z, L == 0), selp(tb.x, tb.z, L == 2), L < 2);
             const unsigned hi = (unsigned)selp(selp(ta.y, ta.w, L == 0), selp(tb.y, tb.w, L == 2), L < 2);
-            const bool more = lo >= 0 && j != 3 && --steps_left != 0;
+            const bool more = lo >= 0 && j != 3 && ++steps != max_steps;
             const int tcur = t;
             const bool d0 = j == 0, d1 = j == 1, d2 = j == 2;
             if (more) {
@@ -752,9 +766,13 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             } else {
                 sum = fma(dz, (double)mut, sum);
             }
-            ++n_cross;
             if (!more) {
-                if (lo >= 0 && j != 3) ++n_stuck;
+                // hull exit (lo < 0), lost (no exit pattern; impossible with
+                // exact signs) or stuck (max_steps crossings)
+                const bool stuck = lo >= 0 && j != 3;
+                n_lost += j == 3 ? 1u : 0u;
+                n_stuck += stuck ? 1u : 0u;
+                n_cross += (unsigned)steps + (stuck ? 0u : 1u);
                 break;
             }
             // mu of the next tet: issued after this step's use so no second
@@ -823,7 +841,8 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
         if (__syncthreads_and(ok)) ax = 2 * kc + (dkc < 0 ? 1 : 0);
     }
     if (e >= 0) {
-#define WALK(AXV) walk_ray<BACK, AXV>(rec, tnode, vtx, ang, beam, a, u, v, rmax, g, max_steps, \
+#define WALK(AXV) walk_ray<BACK, AXV>(rec, tnode, vtx, ang, beam, a, u, v, nu, tw_log, rmax, g, \
+                                      max_steps, \
                                       nverts, e, rid, mu, y, acc, sum, n_cross, n_exact, n_lost, \
                                       n_stuck)
         switch (ax) {
