@@ -146,6 +146,49 @@ struct KernelTimer {
     }
 };
 
+// Side stream for the pipelined host copies of one call, with its events.
+struct CopyStream {
+    cudaStream_t s = nullptr;
+    std::vector<cudaEvent_t> ev;
+    cudaError_t err = cudaSuccess;
+    explicit CopyStream(bool on) {
+        if (on) err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    }
+    cudaError_t event(cudaEvent_t& e) {
+        cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        if (r == cudaSuccess) ev.push_back(e);
+        return r;
+    }
+    // copy stream waits for everything queued on `on` so far
+    cudaError_t after(cudaStream_t on) {
+        cudaEvent_t e;
+        cudaError_t r = event(e);
+        if (r == cudaSuccess) r = cudaEventRecord(e, on);
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(s, e, 0);
+        ev.pop_back();          // only the mark() events are indexed by chunk
+        cudaEventDestroy(e);    // released once the recorded work completes
+        return r;
+    }
+    // event after the last queued copy (ev[k] for the k-th mark)
+    cudaError_t mark() {
+        cudaEvent_t e;
+        cudaError_t r = event(e);
+        return r == cudaSuccess ? cudaEventRecord(e, s) : r;
+    }
+    // `on` waits for every copy queued so far
+    cudaError_t join(cudaStream_t on) {
+        cudaEvent_t e;
+        cudaError_t r = event(e);
+        if (r == cudaSuccess) r = cudaEventRecord(e, s);
+        return r == cudaSuccess ? cudaStreamWaitEvent(on, e, 0) : r;
+    }
+    ~CopyStream() {   // before the scratch it reads is released (also on error paths)
+        if (s) cudaStreamSynchronize(s);
+        for (auto e : ev) cudaEventDestroy(e);
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
 // Shared driver: geometry prep, chunking over angles, entry finder, walker.
 tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, int accumulate,
                Op op, void* stream, tet_stats* st, const tet_options* opt = nullptr) {
@@ -187,12 +230,19 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
     unsigned long long hs[ST_COUNT] = {0};
     {
         Scratch sc(s);  // released (stream-ordered) at the end of this scope
-        // --- stage host inputs / outputs through device memory
+        // --- stage host inputs / outputs through device memory.  The
+        // per-ray host arrays (y of a backprojection, proj of a projection)
+        // move chunk by chunk on a copy stream, overlapped with the tracing
+        // of the neighbouring chunks; the per-tet ones (mu, x) are small.
+        const bool pipe_in = !dev_in && op != Op::Forward;
+        const bool pipe_out = !dev_out && op == Op::Forward;
+        CopyStream cs(pipe_in || pipe_out);
+        if (cs.err != cudaSuccess) return cuda_fail(cs.err, "copy stream");
         const float* d_in = in;
         if (!dev_in) {
             void* p;
             CU(sc.alloc(&p, in_bytes));
-            CU(cudaMemcpyAsync(p, in, in_bytes, cudaMemcpyHostToDevice, s));
+            if (!pipe_in) CU(cudaMemcpyAsync(p, in, in_bytes, cudaMemcpyHostToDevice, s));
             d_in = (const float*)p;
         }
         void* d_out = out;
@@ -222,9 +272,22 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
             CU(sc.alloc((void**)&acc, nt * sizeof(double)));
             CU(cudaMemsetAsync(acc, 0, nt * sizeof(double), s));
         }
-        // --- angle chunks bound the entry-map scratch (<= 2^26 rays per chunk)
+        // --- angle chunks bound the entry-map scratch (<= 2^26 rays per chunk;
+        // 2^23 when host copies are pipelined, for a short prologue/epilogue)
         const int64_t per_angle = (int64_t)g->n_v * g->n_u;
-        const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(g->n_angles, (1LL << 26) / per_angle));
+        const int64_t max_chunk_rays = (pipe_in || pipe_out) ? (1LL << 23) : (1LL << 26);
+        const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(g->n_angles, max_chunk_rays / per_angle));
+        if (pipe_in) {   // all y chunks are queued at once; chunk k's trace waits for its copy
+            CU(cs.after(s));
+            for (int a0 = 0; a0 < g->n_angles; a0 += chunk) {
+                const size_t off = (size_t)a0 * per_angle;
+                const size_t n = (size_t)std::min(chunk, g->n_angles - a0) * per_angle;
+                CU(cudaMemcpyAsync((float*)d_in + off, (const float*)in + off, n * sizeof(float),
+                                   cudaMemcpyHostToDevice, cs.s));
+                CU(cs.mark());
+            }
+        }
+        size_t chunk_idx = 0;
         int* entry;
         CU(sc.alloc((void**)&entry, sizeof(int) * per_angle * chunk));
         void* entry_scratch;
@@ -242,6 +305,8 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
             }
             const size_t off = (size_t)a0 * per_angle;
             const bool fwd = op == Op::Forward;
+            if (pipe_in) CU(cudaStreamWaitEvent(s, cs.ev[chunk_idx], 0));
+            ++chunk_idx;
             if (mode != TET_TRAVERSE_EXACT) {
                 KernelTimer kt(m, fwd ? TET_K_FORWARD : TET_K_BACKWARD, s);
                 CU(launch_mt(m->dev, c, !fwd, mode == TET_TRAVERSE_MT_F32, mto, entry, mu_int,
@@ -254,7 +319,14 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
                 KernelTimer kt(m, TET_K_BACKWARD, s);
                 CU(launch_backward(m->dev, c, entry, d_in + off, acc, d_stats, s));
             }
+            if (pipe_out) {   // this chunk's projections go home while the next one traces
+                CU(cs.after(s));
+                CU(cudaMemcpyAsync((float*)out + off, (float*)d_out + off,
+                                   (size_t)na * per_angle * sizeof(float), cudaMemcpyDeviceToHost,
+                                   cs.s));
+            }
         }
+        if (pipe_out) CU(cs.join(s));
         if (op == Op::Backward) {
             KernelTimer kt(m, TET_K_PERMUTE, s);
             CU(launch_scatter_x(m->dev, acc, (float*)d_out, accumulate, s));
@@ -263,7 +335,7 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
             KernelTimer kt(m, TET_K_PERMUTE, s);
             CU(launch_scatter_acc(m->dev, acc, (double*)d_out, s));
         }
-        if (!dev_out)
+        if (!dev_out && !pipe_out)
             CU(cudaMemcpyAsync(out, d_out, out_elems * sizeof(float), cudaMemcpyDeviceToHost, s));
         if (need_stats) CU(cudaMemcpyAsync(hs, d_stats, sizeof hs, cudaMemcpyDeviceToHost, s));
         CU(cudaGetLastError());
