@@ -262,6 +262,22 @@ __device__ __forceinline__ void xform_ax(const Frame& F, const int4 v, double& x
     }
 }
 
+// Depth z' where the ray (the z' axis) crosses the face (slot 0, 1, 2):
+// barycentric weights |side(1,2)|, |side(2,0)|, |side(0,1)| (all of one exact
+// sign for a crossed face; |.| differs from the exact value only below tau),
+// offsets from slot 0 for accuracy, 1/sum from the MUFU reciprocal refined by
+// one fp64 Newton step (rel. error ~2^-40).  A face with all three weights 0
+// (cannot happen with certified signs) returns `fallback`.
+__device__ __forceinline__ double face_depth(double z0, double z1, double z2, double s01,
+                                             double s12, double s20, double fallback,
+                                             unsigned& n_exact) {
+    const double w0 = fabs(s12), w1 = fabs(s20), w2 = fabs(s01);
+    const double sw = w0 + w1 + w2;
+    if (sw > 0.0) return fma(fma(w1, z1 - z0, w2 * (z2 - z0)), rcp_nr(sw), z0);
+    ++n_exact;
+    return fallback;
+}
+
 __device__ __forceinline__ double side2(double xa, double ya, double xb, double yb) {
     return fma(xa, yb, -(ya * xb));
 }
@@ -675,12 +691,9 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
         xform_ax<AX>(F, __ldg(vtx + id1), x1, y1, z1);
         xform_ax<AX>(F, __ldg(vtx + id2), x2, y2, z2);
         double s01 = side2(x0, y0, x1, y1), s12 = side2(x1, y1, x2, y2), s20 = side2(x2, y2, x0, y0);
-        double zin;
-        {
-            const double w0 = fabs(s12), w1 = fabs(s20), w2 = fabs(s01);
-            const double sw = w0 + w1 + w2;
-            zin = sw > 0 ? (w0 * z0 + w1 * z1 + w2 * z2) / sw : (z0 + z1 + z2) * (1.0 / 3.0);
-        }
+        unsigned n_exact_init = 0;
+        double zin = face_depth(z0, z1, z2, s01, s12, s20, (z0 + z1 + z2) * (1.0 / 3.0),
+                                n_exact_init);
         int steps = 0;   // crossings done before this one
         // Software-pipelined by one step: the gathers of step k+1 (face tags of
         // the next tet, its apex vertex, mu) are issued as soon as step k's
@@ -721,7 +734,6 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             // n_{i+1} = 0; it drops slot j = i+2.  j by table on neg:
             // 1,5 -> i=0, j=2;  2,3 -> i=1, j=0;  4,6 -> i=2, j=1;  0,7 -> lost (3)
             const int j = (int)((kExitLUT >> (2 * neg)) & 3u);
-            const bool c0 = j == 2, c1 = j == 0;
             // exit through the face opposite slot j = i+2 (local index L in t)
             // local index in t of the dropped slot's vertex, from t's node list
             const int idj = selp(id0, selp(id1, id2, j == 1), j == 0);
@@ -738,26 +750,16 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
                 nd = __ldg(tnode + t);
                 X = __ldg(vtx + (int)(hi >> 8));
             }
-            // ---- chord of step k (overlaps the gathers of step k+1)
-            // crossing point weights: apex |s(i,i+1)|, slot i |p_{i+1}|, slot i+1 |p_i|.
-            // Selections are written as predicated moves (IMAD.MOV on the FMA
-            // pipe) rather than FSELs: the ALU pipe is the walker's hot pipe.
-            double si = s20, pi = p2, pn = p0, zi = z2, zn = z0;
-            if (c0) { si = s01; pi = p0; pn = p1; zi = z0; zn = z1; }
-            if (c1) { si = s12; pi = p1; pn = p2; zi = z1; zn = z2; }
-            // all three have exact sign -1/+1/-1; |.| differs from the clamp only when
-            // |value| <= tau (then by <= 2 tau, far below the chord tolerance)
-            const double wA = fabs(si), wQ = fabs(pn), wR = fabs(pi);
-            const double sw = wA + wQ + wR;
-            double zout;
-            if (sw > 0.0) {
-                // offset from the apex; 1/sw from the MUFU reciprocal refined by
-                // one fp64 Newton step (rel. error ~2^-40)
-                zout = fma(fma(wQ, zi - z3, wR * (zn - z3)), rcp_nr(sw), z3);
-            } else {
-                zout = zin;
-                ++n_exact;
-            }
+            // ---- slot update: the apex takes the dropped slot j = i+2 (cyclic
+            // order is preserved); s_{i+1} <- -p_{i+1}, s_{i+2} <- p_i.  The
+            // slots are then the exit face = the next entry face.
+            if (d0) { x0 = x3; y0 = y3; z0 = z3; id0 = iap; s20 = -p2; s01 = p1; }
+            if (d1) { x1 = x3; y1 = y3; z1 = z3; id1 = iap; s01 = -p0; s12 = p2; }
+            if (d2) { x2 = x3; y2 = y3; z2 = z3; id2 = iap; s12 = -p1; s20 = p0; }
+            // ---- chord of step k (overlaps the gathers of step k+1): depth of
+            // the crossing point of the (updated) face, barycentric weights
+            // |s12|, |s20|, |s01| -- symmetric in the slots, so no selects
+            const double zout = face_depth(z0, z1, z2, s01, s12, s20, zin, n_exact);
             // zout - zin >= 0 up to rounding; an exact zero-length crossing
             // may come out as -1e-16 R, which is harmless in the sum
             const double dz = zout - zin;
@@ -779,11 +781,6 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             // register (and no copy that waits on the load) is needed; it is
             // consumed at the end of the next step
             if (!BACK) mut = __ldg(mu + t);
-            // the apex takes the dropped slot i+2 (cyclic order is preserved);
-            // s_{i+1} <- -p_{i+1}, s_{i+2} <- p_i
-            if (d0) { x0 = x3; y0 = y3; z0 = z3; id0 = iap; s20 = -p2; s01 = p1; }
-            if (d1) { x1 = x3; y1 = y3; z1 = z3; id1 = iap; s01 = -p0; s12 = p2; }
-            if (d2) { x2 = x3; y2 = y3; z2 = z3; id2 = iap; s12 = -p1; s20 = p0; }
             zin = zout;
             iap = (int)(hi >> 8);
         }
