@@ -262,25 +262,27 @@ __device__ __forceinline__ void xform_ax(const Frame& F, const int4 v, double& x
     }
 }
 
+__device__ __forceinline__ double side2(double xa, double ya, double xb, double yb) {
+    return fma(xa, yb, -(ya * xb));
+}
+
 // Depth z' where the ray (the z' axis) crosses the face (slot 0, 1, 2):
 // barycentric weights |side(1,2)|, |side(2,0)|, |side(0,1)| (all of one exact
 // sign for a crossed face; |.| differs from the exact value only below tau),
 // offsets from slot 0 for accuracy, 1/sum from the MUFU reciprocal refined by
 // one fp64 Newton step (rel. error ~2^-40).  A face with all three weights 0
 // (cannot happen with certified signs) returns `fallback`.
-__device__ __forceinline__ double face_depth(double z0, double z1, double z2, double s01,
-                                             double s12, double s20, double fallback,
-                                             unsigned& n_exact) {
-    const double w0 = fabs(s12), w1 = fabs(s20), w2 = fabs(s01);
+__device__ __forceinline__ double face_depth(double x0, double y0, double z0, double x1,
+                                             double y1, double z1, double x2, double y2,
+                                             double z2, double fallback, unsigned& n_exact) {
+    const double w0 = fabs(side2(x1, y1, x2, y2)), w1 = fabs(side2(x2, y2, x0, y0)),
+                 w2 = fabs(side2(x0, y0, x1, y1));
     const double sw = w0 + w1 + w2;
     if (sw > 0.0) return fma(fma(w1, z1 - z0, w2 * (z2 - z0)), rcp_nr(sw), z0);
     ++n_exact;
     return fallback;
 }
 
-__device__ __forceinline__ double side2(double xa, double ya, double xb, double yb) {
-    return fma(xa, yb, -(ya * xb));
-}
 
 __device__ __forceinline__ int sel4(int4 v, int k) {
     return selp(selp(v.x, v.y, k == 0), selp(v.z, v.w, k == 2), k < 2);
@@ -651,12 +653,12 @@ __device__ __forceinline__ bool any_abs_le(double a, double b, double c, double 
 
 // One thread per ray, 8x4-pixel warp tiles (16x8 per block).
 // State: the entry face in three fixed slots k = 0,1,2 in cyclic order (shear
-// coordinates x', y', z', vertex id, local index l_k in the current tet) with
-// the edge sides s01, s12, s20 (exact sign -1), the apex id `iap` (from the
-// previous face tag), the entry depth zin.  Per step the face tags of t and
-// the apex vertex are gathered IN PARALLEL (the tag carried the apex id);
-// the tag of the exit face gives the next tet, its apex and the local-index
-// map, so the neighbour's node list is never loaded.
+// coordinates x', y', z' and vertex id), the apex id `iap` (from the previous
+// face tag) and the entry depth zin.  Per step the face tags and node ids of
+// t and the apex vertex are gathered IN PARALLEL (the previous tag carried the
+// apex id); the sign code of the three sides side(apex, slot k) picks the
+// exit face, t's node list gives its local index, and that face's tag gives
+// the next tet and its apex.
 template <bool BACK, int AX>
 __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int4* __restrict__ tnode,
                                          const int4* __restrict__ vtx,
@@ -690,9 +692,8 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
         xform_ax<AX>(F, __ldg(vtx + id0), x0, y0, z0);
         xform_ax<AX>(F, __ldg(vtx + id1), x1, y1, z1);
         xform_ax<AX>(F, __ldg(vtx + id2), x2, y2, z2);
-        double s01 = side2(x0, y0, x1, y1), s12 = side2(x1, y1, x2, y2), s20 = side2(x2, y2, x0, y0);
         unsigned n_exact_init = 0;
-        double zin = face_depth(z0, z1, z2, s01, s12, s20, (z0 + z1 + z2) * (1.0 / 3.0),
+        double zin = face_depth(x0, y0, z0, x1, y1, z1, x2, y2, z2, (z0 + z1 + z2) * (1.0 / 3.0),
                                 n_exact_init);
         int steps = 0;   // crossings done before this one
         // Software-pipelined by one step: the gathers of step k+1 (face tags of
@@ -753,13 +754,13 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             // ---- slot update: the apex takes the dropped slot j = i+2 (cyclic
             // order is preserved); s_{i+1} <- -p_{i+1}, s_{i+2} <- p_i.  The
             // slots are then the exit face = the next entry face.
-            if (d0) { x0 = x3; y0 = y3; z0 = z3; id0 = iap; s20 = -p2; s01 = p1; }
-            if (d1) { x1 = x3; y1 = y3; z1 = z3; id1 = iap; s01 = -p0; s12 = p2; }
-            if (d2) { x2 = x3; y2 = y3; z2 = z3; id2 = iap; s12 = -p1; s20 = p0; }
+            if (d0) { x0 = x3; y0 = y3; z0 = z3; id0 = iap; }
+            if (d1) { x1 = x3; y1 = y3; z1 = z3; id1 = iap; }
+            if (d2) { x2 = x3; y2 = y3; z2 = z3; id2 = iap; }
             // ---- chord of step k (overlaps the gathers of step k+1): depth of
             // the crossing point of the (updated) face, barycentric weights
             // |s12|, |s20|, |s01| -- symmetric in the slots, so no selects
-            const double zout = face_depth(z0, z1, z2, s01, s12, s20, zin, n_exact);
+            const double zout = face_depth(x0, y0, z0, x1, y1, z1, x2, y2, z2, zin, n_exact);
             // zout - zin >= 0 up to rounding; an exact zero-length crossing
             // may come out as -1e-16 R, which is harmless in the sum
             const double dz = zout - zin;
@@ -1105,6 +1106,13 @@ static dim3 trace_grid_w(const LaunchChunk& c, int tw_log) {
 // 4 resident 128-thread blocks per SM (128 registers, no spills).  Capping the
 // registers for 5 or 6 blocks spills inside the loop and was measured slower
 // (DESIGN.md §5).
+// Blocks per SM the walker is compiled for (register cap 65536 / (128 x n)):
+// the forward walk is fastest at 6 (80 registers, a few loop-invariant spills,
+// 24 warps/SM), the backward walk at 4 (128 registers, no spills) -- its
+// spilled values feed the RED atomics and stall them (profiles/README.md).
+template <bool BACK>
+constexpr int kTraceMinBlocks = BACK ? 4 : 6;
+
 template <bool BACK>
 static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entry,
                          const float* mu_int, float* proj, const float* y, double* acc,
@@ -1112,7 +1120,7 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
     const int twl = tile_w_log();
     if (m.l2_window_bytes == 0) {
-        trace_kernel<BACK, 4><<<trace_grid_w(c, twl), 128, 0, s>>>(TRACE_ARGS, twl, (int)m.nv);
+        trace_kernel<BACK, kTraceMinBlocks<BACK>><<<trace_grid_w(c, twl), 128, 0, s>>>(TRACE_ARGS, twl, (int)m.nv);
         return;
     }
     // L2 persistence hint for the face-tag records (per launch; the caller's
@@ -1130,7 +1138,7 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, trace_kernel<BACK, 4>, TRACE_ARGS, twl, (int)m.nv);
+    cudaLaunchKernelEx(&cfg, trace_kernel<BACK, kTraceMinBlocks<BACK>>, TRACE_ARGS, twl, (int)m.nv);
 }
 
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
