@@ -28,6 +28,10 @@ import numpy as np  # noqa: E402
 METRIC = "tet-crossings/s (fwd+back step)"
 BYTES_FWD = 52   # gathered bytes per crossing, forward
 BYTES_BACK = 56  # gathered bytes per crossing, backward with f64 accumulator
+# compulsory bytes per crossing: apex id + coords + exit id + mu
+# forward; + f64 accumulator read-modify-write backward
+COMPULSORY_FWD = 24
+COMPULSORY_BACK = 36
 
 
 def parse():
@@ -122,6 +126,16 @@ def measured_peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def l2_gather_peak():
+    """Measured random 32-B gather rate from L2 (experiments/microbench.py,
+    profiles/r01_microbench.json): the second denominator of SURVEY §8(d)."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "profiles", "r01_microbench.json")))
+                     ["gather32_L2_GBps"])
+    except Exception:
+        return None
 
 
 def ncu_traffic(kernel, crossings_per_launch):
@@ -336,6 +350,8 @@ def main():
             dom, bytes_unit, cross_unit, launches, tdom = "backward", BYTES_BACK, st_b["crossings"], nb, tb
         else:
             dom, bytes_unit, cross_unit, launches, tdom = "forward", BYTES_FWD, st_f["crossings"], nf, tf
+        comp_unit = COMPULSORY_BACK if dom == "backward" else COMPULSORY_FWD
+        l2pk = l2_gather_peak()
         algo_bytes_per_launch = bytes_unit * cross_unit / max(launches // args.steps, 1)
         achieved = algo_bytes_per_launch / (tdom / max(launches, 1) / 1e3) / 1e9
         # each timed entry region launches two kernels (setup + raster)
@@ -376,7 +392,12 @@ def main():
                          "traffic": ncu_traffic(dom, cross_unit / max(launches // args.steps, 1))
                          if args.config == "c3" else None,
                          "per_launch_ms": per_launch_b if dom == "backward" else per_launch_f,
-                         "note": "gathered bytes per crossing x crossings / walk-kernel time"},
+                         "note": "gathered bytes per crossing x crossings / walk-kernel time; "
+                                 "the c3 working set is L2-resident (DESIGN.md §5 Roofline)",
+                         "compulsory_bytes_per_crossing": comp_unit,
+                         "compulsory_frac": achieved * comp_unit / bytes_unit / peak,
+                         "l2_gather_peak_gbs": l2pk,
+                         "l2_gather_frac": achieved / l2pk if l2pk else None},
             "e2e": {"value": e2e_value, "unit": "tet-crossings/s",
                     "h2d_bytes_per_step": int(w.mu.nbytes + y_np.nbytes),
                     "d2h_bytes_per_step": int(proj.numel() * 4 + x.numel() * 4)},
