@@ -702,7 +702,6 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
         // run while they are in flight.
         int4 ta, tb;
         ldg_rec256(rec + 2 * (size_t)t, ta, tb);             // face tags of t (32 B)
-        int4 nd = nodes;                                     // node ids of t (16 B)
         float mut = 0.f;
         if (!BACK) mut = __ldg(mu + t);
         int4 X = __ldg(vtx + iap);                          // apex vertex (16 B)
@@ -736,20 +735,20 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             // 1,5 -> i=0, j=2;  2,3 -> i=1, j=0;  4,6 -> i=2, j=1;  0,7 -> lost (3)
             const int j = (int)((kExitLUT >> (2 * neg)) & 3u);
             // exit through the face opposite slot j = i+2 (local index L in t)
-            // local index in t of the dropped slot's vertex, from t's node list
+            // the exit face is stored at the rank of the dropped slot's vertex
+            // id among t's four vertex ids (three slots + apex), mesh_host.cpp
             const int idj = selp(id0, selp(id1, id2, j == 1), j == 0);
-            const int L = selp(0, selp(1, selp(2, 3, idj == nd.z), idj == nd.y), idj == nd.x);
+            const int L = (id0 < idj) + (id1 < idj) + (id2 < idj) + (iap < idj);
             const int lo = selp(selp(ta.x, ta.z, L == 0), selp(tb.x, tb.z, L == 2), L < 2);
             const unsigned hi = (unsigned)selp(selp(ta.y, ta.w, L == 0), selp(tb.y, tb.w, L == 2), L < 2);
             const bool more = lo >= 0 && j != 3 && ++steps != max_steps;
             const int tcur = t;
             const bool d0 = j == 0, d1 = j == 1, d2 = j == 2;
             if (more) {
-                t = lo >> 2;
-                DBG_CHECK(t >= 0 && t < max_steps && (int)(hi >> 8) < nverts);
+                t = lo;
+                DBG_CHECK(t >= 0 && t < max_steps && (int)hi >= 0 && (int)hi < nverts);
                 ldg_rec256(rec + 2 * (size_t)t, ta, tb);
-                nd = __ldg(tnode + t);
-                X = __ldg(vtx + (int)(hi >> 8));
+                X = __ldg(vtx + (int)hi);
             }
             // ---- slot update: the apex takes the dropped slot j = i+2 (cyclic
             // order is preserved); s_{i+1} <- -p_{i+1}, s_{i+2} <- p_i.  The
@@ -783,7 +782,7 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             // consumed at the end of the next step
             if (!BACK) mut = __ldg(mu + t);
             zin = zout;
-            iap = (int)(hi >> 8);
+            iap = (int)hi;
         }
         if (!BACK) sum *= F.scale;
     }
@@ -977,10 +976,16 @@ __global__ void __launch_bounds__(128) mt_trace_kernel(const int4* __restrict__ 
             ++n_cross;
             // neighbour of the face where t2 happened; "if t2 = t1 check if they
             // need to be swapped": do not step back into the previous element
+            // (face tags are stored by the rank of the opposite vertex id)
             const int4 r0 = __ldg(rec + 2 * (size_t)t), r1v = __ldg(rec + 2 * (size_t)t + 1);
             const int nb[4] = {r0.x, r0.z, r1v.x, r1v.z};
-            int nxt = nb[kmax] < 0 ? -1 : (nb[kmax] >> 2);
-            if (tmax == tmin && nxt == prev && kmin != kmax) nxt = nb[kmin] < 0 ? -1 : (nb[kmin] >> 2);
+            auto rank = [&](int k) {
+                int r = 0;
+                for (int q = 0; q < 4; ++q) r += ids[q] < ids[k];
+                return r;
+            };
+            int nxt = nb[rank(kmax)];
+            if (tmax == tmin && nxt == prev && kmin != kmax) nxt = nb[rank(kmin)];
             prev = t;
             t = nxt;
             if (++steps >= max_steps) { ++n_stuck; break; }

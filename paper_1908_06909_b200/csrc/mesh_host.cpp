@@ -378,41 +378,35 @@ tet_status prepare_mesh(const double* verts, int64_t nv, const int32_t* tets,
         br2 = std::max(br2, s);
     }
     M.bs_r = std::sqrt(br2) * (1 + 1e-12) + 1;
-    // Face tags: face k of tet t -> two int32 words
-    //   lo = n<<2 | k'            (n = neighbour, k' = shared face's local index
-    //                              in n = local index of n's apex); -1 on the hull
-    //   hi = apex<<8 | map        (apex = vertex id of node k' of n; map holds,
-    //                              2 bits per t-local index j != k, the n-local
-    //                              index of node j of t)
-    // so the walker gets the next apex and the slots' local indices without
-    // loading the neighbour's node list.
-    if (nvu > (1 << 23)) { err = "more than 2^23 vertices (face-tag apex field)"; return TET_E_MESH; }
+    // Face tags: face k of tet t (opposite node k) -> two int32
+    // words, stored at position r = rank of node k's vertex id among the
+    // tet's four (new) vertex ids:
+    //   lo = n     (neighbour across the face, internal index); -1 on the hull
+    //   hi = apex  (vertex id of n's node opposite the shared face); -1 on the hull
+    // The walker holds all four vertex ids of t (three face slots + apex), so
+    // it finds the exit face's position by ranking the dropped vertex among
+    // them -- no node list or local-index bookkeeping in the loop -- and the
+    // tag gives the next tet and its apex (gathered one step ahead).
     M.rec.assign((size_t)nt * 8, 0);
     M.tnode.assign((size_t)nt * 4, 0);
     M.perm.assign(nt, 0);
     for (int64_t i = 0; i < nt; ++i) {
         int64_t t = order[i];
         M.perm[i] = (int32_t)t;
+        int32_t ids[4];
+        for (int k = 0; k < 4; ++k) ids[k] = M.tnode[4 * i + k] = vnew[T[4 * t + k]];
         for (int k = 0; k < 4; ++k) {
-            M.tnode[4 * i + k] = vnew[T[4 * t + k]];
+            int r = 0;
+            for (int j = 0; j < 4; ++j) r += ids[j] < ids[k];
             int32_t n = N[4 * t + k];
             if (n < 0) {
-                M.rec[8 * i + 2 * k] = -1;
-                M.rec[8 * i + 2 * k + 1] = -1;
+                M.rec[8 * i + 2 * r] = -1;
+                M.rec[8 * i + 2 * r + 1] = -1;
                 continue;
             }
             const int kp = kback[4 * t + k];
-            uint32_t map = 0;
-            for (int j = 0; j < 4; ++j) {
-                if (j == k) continue;
-                int m = -1;
-                for (int jj = 0; jj < 4; ++jj)
-                    if (T[4 * (int64_t)n + jj] == T[4 * t + j]) m = jj;
-                map |= (uint32_t)m << (2 * j);
-            }
-            const uint32_t apex = (uint32_t)vnew[T[4 * (int64_t)n + kp]];
-            M.rec[8 * i + 2 * k] = (inv[n] << 2) | kp;
-            M.rec[8 * i + 2 * k + 1] = (int32_t)((apex << 8) | map);
+            M.rec[8 * i + 2 * r] = inv[n];
+            M.rec[8 * i + 2 * r + 1] = vnew[T[4 * (int64_t)n + kp]];
         }
     }
     M.hull.resize((size_t)B * 2);
