@@ -354,6 +354,7 @@ def main():
         l2pk = l2_gather_peak()
         algo_bytes_per_launch = bytes_unit * cross_unit / max(launches // args.steps, 1)
         achieved = algo_bytes_per_launch / (tdom / max(launches, 1) / 1e3) / 1e9
+        achieved_c = achieved * comp_unit / bytes_unit
         # each timed entry region launches two kernels (setup + raster)
         n_launch_step = (nf + nb + 2 * ne + np_) / args.steps
         clk = clocks.summary()
@@ -386,16 +387,19 @@ def main():
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
             "mesh_create_s": t_create,
             "roofline": {"bound": "hbm", "kernel": f"trace_kernel<{dom}>",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_source": peak_src,
-                         "bytes_per_crossing": bytes_unit,
+                         "achieved": achieved_c, "peak": peak, "unit": "GB/s",
+                         "frac": achieved_c / peak, "peak_source": peak_src,
+                         "bytes_per_crossing": comp_unit,
                          "traffic": ncu_traffic(dom, cross_unit / max(launches // args.steps, 1))
                          if args.config == "c3" else None,
                          "per_launch_ms": per_launch_b if dom == "backward" else per_launch_f,
-                         "note": "gathered bytes per crossing x crossings / walk-kernel time; "
-                                 "the c3 working set is L2-resident (DESIGN.md §5 Roofline)",
-                         "compulsory_bytes_per_crossing": comp_unit,
-                         "compulsory_frac": achieved * comp_unit / bytes_unit / peak,
+                         "note": "compulsory bytes per crossing (SURVEY 8(d)) x crossings / "
+                                 "walk-kernel time; the c3 working set is L2-resident, so DRAM "
+                                 "traffic is ~0.15 B/crossing and the walk is latency/issue-bound "
+                                 "(DESIGN.md 5, Roofline)",
+                         "gathered_bytes_per_crossing": bytes_unit,
+                         "gathered_achieved": achieved,
+                         "gathered_frac": achieved / peak,
                          "l2_gather_peak_gbs": l2pk,
                          "l2_gather_frac": achieved / l2pk if l2pk else None},
             "e2e": {"value": e2e_value, "unit": "tet-crossings/s",
