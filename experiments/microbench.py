@@ -6,6 +6,8 @@
   stream_L2     coalesced reads of a 64 MB buffer, 50 passes (L2 bandwidth)
   dfma          fp64 FMA rate (8 independent chains per thread)
   red_f64       RED.ADD.F64 to random addresses of an 8 MB array (L2 atomics)
+  red_f32       RED.ADD.F32, same pattern
+  red_*_coherent  8 addresses x 4 lanes per warp instruction (the walker's pattern)
 
 Prints one JSON object; copied to profiles/ as rNN_microbench.json.
 """
@@ -50,6 +52,12 @@ def main():
     it = 64
     ms = L.tetmicro_run(3, 8 << 20, it, sms * 16, 256)
     out["red_f64_Gops"] = sms * 16 * 256 * it / (ms / 1e3) / 1e9
+    ms = L.tetmicro_run(4, 8 << 20, it, sms * 16, 256)
+    out["red_f32_Gops"] = sms * 16 * 256 * it / (ms / 1e3) / 1e9
+    ms = L.tetmicro_run(5, 8 << 20, it, sms * 16, 256)
+    out["red_f64_coherent_Gops"] = sms * 16 * 256 * it / (ms / 1e3) / 1e9
+    ms = L.tetmicro_run(6, 8 << 20, it, sms * 16, 256)
+    out["red_f32_coherent_Gops"] = sms * 16 * 256 * it / (ms / 1e3) / 1e9
     print(json.dumps(out))
     path = os.path.join(ROOT, "gpurun_out", "microbench.json")
     os.makedirs(os.path.dirname(path), exist_ok=True)

@@ -68,12 +68,31 @@ __global__ void red_kernel(double* __restrict__ acc, uint64_t n, int iters) {
     for (int i = 0; i < iters; ++i) atomicAdd(acc + hash32(tid * 31u + i * 0x85ebca6bu) % n, 1.0);
 }
 
+// REDs with the walker's pattern: per iteration a warp picks one random base
+// and lane l adds to base + (l >> 2) (8 addresses per warp instruction, 4
+// lanes on each -- coherent rays crossing the same tets).
+template <typename T>
+__global__ void red_coherent_kernel(T* __restrict__ acc, uint64_t n, int iters) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t warp = tid >> 5, lane = tid & 31;
+    for (int i = 0; i < iters; ++i) {
+        const uint64_t base = hash32(warp * 31u + i * 0x85ebca6bu) % (n - 8);
+        atomicAdd(acc + base + (lane >> 2), (T)1);
+    }
+}
+
+__global__ void red32_kernel(float* __restrict__ acc, uint64_t n, int iters) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int i = 0; i < iters; ++i) atomicAdd(acc + hash32(tid * 31u + i * 0x85ebca6bu) % n, 1.0f);
+}
+
 }  // namespace
 
 extern "C" {
 
 // Returns the kernel time in ms (CUDA events), or a negative value on error.
-// kind: 0 gather32 (bytes = n_rec_used*32 buffer), 1 stream, 2 dfma, 3 red.f64
+// kind: 0 gather32 (bytes = n_rec_used*32 buffer), 1 stream, 2 dfma, 3 red.f64,
+// 4 red.f32, 5 red.f64 coherent (8 addresses x 4 lanes per warp), 6 red.f32 coherent
 double tetmicro_run(int kind, uint64_t buffer_bytes, int iters, int blocks, int threads) {
     void* buf = nullptr;
     unsigned* sink = nullptr;
@@ -91,8 +110,14 @@ double tetmicro_run(int kind, uint64_t buffer_bytes, int iters, int blocks, int 
             stream_kernel<<<blocks, threads>>>((const int4*)buf, buffer_bytes / 16, iters, sink);
         else if (kind == 2)
             dfma_kernel<<<blocks, threads>>>((double*)buf, iters);
-        else
+        else if (kind == 3)
             red_kernel<<<blocks, threads>>>((double*)buf, buffer_bytes / 8, iters);
+        else if (kind == 4)
+            red32_kernel<<<blocks, threads>>>((float*)buf, buffer_bytes / 4, iters);
+        else if (kind == 5)
+            red_coherent_kernel<double><<<blocks, threads>>>((double*)buf, buffer_bytes / 8, iters);
+        else
+            red_coherent_kernel<float><<<blocks, threads>>>((float*)buf, buffer_bytes / 4, iters);
         cudaEventRecord(b);
     }
     cudaEventSynchronize(b);
