@@ -247,6 +247,55 @@ def test_full_size_c3_sampled():
     assert abs(rowsum - colsum) / rowsum <= U.ADJ_TOL
 
 
+def _sampled_backprojection_check(tm, geom, mesh, om, ids):
+    """Backprojection per tet at full size: y = 1 + (ray id mod 7) on the
+    sampled rays and 0 elsewhere, so the oracle computes every tet's exact
+    value from those rays alone (oracle backproject with ray_ids)."""
+    import torch
+
+    from oracle import tetref as O
+    y = np.zeros(geom.n_rays, np.float32)
+    y[ids] = 1.0 + (ids % 7).astype(np.float32)
+    x = tm.backproject(geom, torch.from_numpy(y).cuda()).cpu().numpy().astype(np.float64)
+    xr, _ = O.backproject(om, geom, y[ids], ray_ids=ids)
+    assert np.count_nonzero(xr) > 1000
+    be = U.back_errors(x, xr)
+    assert be.max() <= U.BACK_TOL, (be.max(), int(be.argmax()))
+
+
+def test_full_size_c3_sampled_backprojection():
+    """c3 at full size: every tet's backprojection of 3000 sampled rays."""
+    from oracle import tetref as O
+    from paper_1908_06909_b200 import tetproj as T
+    w = CF.workload("c3")
+    tm = T.TetMesh.from_mesh(w.mesh)
+    om = O.OracleMesh.from_mesh(w.mesh)
+    ids = np.sort(np.random.default_rng(11).choice(w.geom.n_rays, 3000, replace=False))
+    _sampled_backprojection_check(tm, w.geom, w.mesh, om, ids)
+
+
+def test_full_size_c5_mesh_sampled():
+    """BASELINE config c5's 10.5 M-tet mesh at its full 1024^2 detector (8 of
+    the 720 angles, evenly spaced -- the per-GPU work is angle-sharded): 2000
+    sampled rays' projections one by one, every tet's backprojection of those
+    rays, zero lost / stuck rays."""
+    import torch
+
+    from oracle import tetref as O
+    from paper_1908_06909_b200 import tetproj as T
+    w = CF.workload("c5")
+    geom = w.geom.subset(np.arange(0, w.geom.n_angles, w.geom.n_angles // 8))
+    tm = T.TetMesh.from_mesh(w.mesh)
+    p, st = tm.project(geom, torch.from_numpy(w.mu).cuda(), stats=True)
+    assert st["lost"] == st["stuck"] == st["entry_conflicts"] == 0, st
+    om = O.OracleMesh.from_mesh(w.mesh)
+    ids = np.sort(np.random.default_rng(5).choice(geom.n_rays, 2000, replace=False))
+    pr, ost = O.project(om, geom, w.mu.astype(np.float64), ray_ids=ids)
+    fe = U.fwd_errors(p.cpu().numpy().ravel()[ids].astype(np.float64), pr, w.mu, w.mesh)
+    assert fe.max() <= U.FWD_TOL, fe.max()
+    _sampled_backprojection_check(tm, geom, w.mesh, om, ids)
+
+
 def test_paper_mt_modes_run_and_agree_on_generic_rays():
     """NEXT-1: the paper's Alg. 1/2 walker (fp64) agrees with the exact walker
     on generic rays of the ball mesh; fp32 runs and reports its failures."""
