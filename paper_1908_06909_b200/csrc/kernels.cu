@@ -654,11 +654,12 @@ __device__ __forceinline__ bool any_abs_le(double a, double b, double c, double 
 // One thread per ray, 8x4-pixel warp tiles (16x8 per block).
 // State: the entry face in three fixed slots k = 0,1,2 in cyclic order (shear
 // coordinates x', y', z' and vertex id), the apex id `iap` (from the previous
-// face tag) and the entry depth zin.  Per step the face tags and node ids of
-// t and the apex vertex are gathered IN PARALLEL (the previous tag carried the
-// apex id); the sign code of the three sides side(apex, slot k) picks the
-// exit face, t's node list gives its local index, and that face's tag gives
-// the next tet and its apex.
+// face tag) and the entry depth zin.  Per step the face tags of t and the
+// apex vertex are gathered IN PARALLEL (the previous tag carried the apex
+// id); the sign code of the three sides side(apex, slot k) picks the exit
+// face, the rank of the dropped slot's vertex id among t's four ids gives the
+// position of its tag, and the tag gives the next tet and its apex
+// (DESIGN.md §5).
 template <bool BACK, int AX>
 __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int4* __restrict__ tnode,
                                          const int4* __restrict__ vtx,
@@ -734,8 +735,8 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             // n_{i+1} = 0; it drops slot j = i+2.  j by table on neg:
             // 1,5 -> i=0, j=2;  2,3 -> i=1, j=0;  4,6 -> i=2, j=1;  0,7 -> lost (3)
             const int j = (int)((kExitLUT >> (2 * neg)) & 3u);
-            // exit through the face opposite slot j = i+2 (local index L in t)
-            // the exit face is stored at the rank of the dropped slot's vertex
+            // exit through the face opposite slot j = i+2; its tag is stored at
+            // the rank of the dropped slot's vertex
             // id among t's four vertex ids (three slots + apex), mesh_host.cpp
             const int idj = selp(id0, selp(id1, id2, j == 1), j == 0);
             const int L = (id0 < idj) + (id1 < idj) + (id2 < idj) + (iap < idj);
