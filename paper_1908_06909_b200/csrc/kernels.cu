@@ -98,21 +98,24 @@ __device__ __noinline__ int exact_side_ids(const int4* __restrict__ vtx,
 // The walker's rare exact path: the thread's own ray is recomputed from its
 // grid position (same mapping as trace_kernel), so (a, u, v) need not stay
 // live in registers across the walk loop.
+// Walker blocks are BX x BY warp tiles of (1 << tw_log) x (32 >> tw_log) pixels.
+template <int BX, int BY>
 __device__ __forceinline__ void thread_pixel(int nu, int tw_log, int& a, int& u, int& v) {
     const int tw = 1 << tw_log, th = 32 >> tw_log;
-    const int tiles_u = (nu + 2 * tw - 1) / (2 * tw);
+    const int tiles_u = (nu + BX * tw - 1) / (BX * tw);
     const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     a = blockIdx.y;
-    u = bx * 2 * tw + (w & 1) * tw + (lane & (tw - 1));
-    v = by * 2 * th + (w >> 1) * th + (lane >> tw_log);
+    u = bx * BX * tw + (w % BX) * tw + (lane & (tw - 1));
+    v = by * BY * th + (w / BX) * th + (lane >> tw_log);
 }
 
+template <int BX, int BY>
 __device__ __noinline__ int exact_side_here(const int4* __restrict__ vtx,
                                             const AngleGeom* __restrict__ ang, int beam, int nu,
                                             int tw_log, int ia, int ib) {
     int a, u, v;
-    thread_pixel(nu, tw_log, a, u, v);
+    thread_pixel<BX, BY>(nu, tw_log, a, u, v);
     return exact_side_ids(vtx, ang, beam, a, u, v, ia, ib);
 }
 
@@ -660,7 +663,7 @@ __device__ __forceinline__ bool any_abs_le(double a, double b, double c, double 
 // face, the rank of the dropped slot's vertex id among t's four ids gives the
 // position of its tag, and the tag gives the next tet and its apex
 // (DESIGN.md §5).
-template <bool BACK, int AX>
+template <bool BACK, int AX, int BX, int BY>
 __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int4* __restrict__ tnode,
                                          const int4* __restrict__ vtx,
                                          const AngleGeom* __restrict__ ang, int beam, int a, int u,
@@ -726,9 +729,9 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             if (any_abs_le(p0, p1, p2, F.tau)) {
                 const unsigned m = neg;
                 neg = 0;
-                neg |= fabs(p0) <= F.tau ? (exact_side_here(vtx, ang, beam, nu, tw_log, iap, id0) < 0 ? 1u : 0u) : (m & 1u);
-                neg |= fabs(p1) <= F.tau ? (exact_side_here(vtx, ang, beam, nu, tw_log, iap, id1) < 0 ? 2u : 0u) : (m & 2u);
-                neg |= fabs(p2) <= F.tau ? (exact_side_here(vtx, ang, beam, nu, tw_log, iap, id2) < 0 ? 4u : 0u) : (m & 4u);
+                neg |= fabs(p0) <= F.tau ? (exact_side_here<BX, BY>(vtx, ang, beam, nu, tw_log, iap, id0) < 0 ? 1u : 0u) : (m & 1u);
+                neg |= fabs(p1) <= F.tau ? (exact_side_here<BX, BY>(vtx, ang, beam, nu, tw_log, iap, id1) < 0 ? 2u : 0u) : (m & 2u);
+                neg |= fabs(p2) <= F.tau ? (exact_side_here<BX, BY>(vtx, ang, beam, nu, tw_log, iap, id2) < 0 ? 4u : 0u) : (m & 4u);
                 n_exact += (fabs(p0) <= F.tau) + (fabs(p1) <= F.tau) + (fabs(p2) <= F.tau);
             }
             // exit face (apex, slot i, slot i+1) for the unique i with n_i = 1,
@@ -788,8 +791,8 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
         if (!BACK) sum *= F.scale;
     }
 
-template <bool BACK, int MINB>
-__global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict__ rec,
+template <bool BACK, int BX, int BY, int MINB>
+__global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* __restrict__ rec,
                                                           const int4* __restrict__ tnode,
                                                           const int4* __restrict__ vtx,
                                                           const AngleGeom* __restrict__ ang,
@@ -804,12 +807,12 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
                                                           int tw_log, int nverts) {
     // warp tile: (1 << tw_log) x (32 >> tw_log) pixels; block = 2 x 2 warp tiles
     const int tw = 1 << tw_log, th = 32 >> tw_log;
-    const int tiles_u = (nu + 2 * tw - 1) / (2 * tw);
+    const int tiles_u = (nu + BX * tw - 1) / (BX * tw);
     const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
     const int a = blockIdx.y;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int u = bx * 2 * tw + (w & 1) * tw + (lane & (tw - 1));
-    const int v = by * 2 * th + (w >> 1) * th + (lane >> tw_log);
+    const int u = bx * BX * tw + (w % BX) * tw + (lane & (tw - 1));
+    const int v = by * BY * th + (w / BX) * th + (lane >> tw_log);
     const bool valid = u < nu && v < nv;
     const size_t rid = ((size_t)a * nv + v) * nu + u;
     const int e = valid ? entry[rid] : -1;
@@ -821,7 +824,8 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
     // sign (block vote), else the generic per-ray frame (variant 6) is used.
     int ax = 6;
     {
-        const int uc = min(bx * 2 * tw + tw, nu - 1), vc = min(by * 2 * th + th, nv - 1);
+        const int uc = min(bx * BX * tw + BX * tw / 2, nu - 1);
+        const int vc = min(by * BY * th + BY * th / 2, nv - 1);
         const RayPts rc = ray_points(ang[a], beam, uc, vc);
         const long long cx = rc.px - rc.ox, cy = rc.py - rc.oy, cz = rc.pz - rc.oz;
         const long long ax_ = cx < 0 ? -cx : cx, ay_ = cy < 0 ? -cy : cy, az_ = cz < 0 ? -cz : cz;
@@ -839,7 +843,7 @@ __global__ void __launch_bounds__(128, MINB) trace_kernel(const int4* __restrict
         if (__syncthreads_and(ok)) ax = 2 * kc + (dkc < 0 ? 1 : 0);
     }
     if (e >= 0) {
-#define WALK(AXV) walk_ray<BACK, AXV>(rec, tnode, vtx, ang, beam, a, u, v, nu, tw_log, rmax, g, \
+#define WALK(AXV) walk_ray<BACK, AXV, BX, BY>(rec, tnode, vtx, ang, beam, a, u, v, nu, tw_log, rmax, g, \
                                       max_steps, \
                                       nverts, e, rid, mu, y, acc, sum, n_cross, n_exact, n_lost, \
                                       n_stuck)
@@ -1100,40 +1104,57 @@ static int tile_w_log() {
     return v;
 }
 
-static dim3 trace_grid_w(const LaunchChunk& c, int tw_log) {
+static dim3 trace_grid_w(const LaunchChunk& c, int tw_log, int bx, int by) {
     const int tw = 1 << tw_log, th = 32 >> tw_log;
-    const unsigned tiles = (unsigned)(((c.nu + 2 * tw - 1) / (2 * tw)) * ((c.nv + 2 * th - 1) / (2 * th)));
+    const unsigned tiles = (unsigned)(((c.nu + bx * tw - 1) / (bx * tw)) *
+                                      ((c.nv + by * th - 1) / (by * th)));
     return dim3(tiles, (unsigned)c.n_angles);
 }
 
 #define TRACE_ARGS m.rec, m.tnode, m.vtx, c.ang, c.beam, c.nv, c.nu, m.rmax, m.g, steps, entry, \
                    mu_int, proj, y, acc, stats
 
-// 4 resident 128-thread blocks per SM (128 registers, no spills).  Capping the
-// registers for 5 or 6 blocks spills inside the loop and was measured slower
-// (DESIGN.md §5).
-// Blocks per SM the walker is compiled for (register cap 65536 / (128 x n)):
-// the forward walk is fastest at 6 (80 registers, a few loop-invariant spills,
-// 24 warps/SM), the backward walk at 4 (128 registers, no spills) -- its
-// spilled values feed the RED atomics and stall them (profiles/README.md).
-template <bool BACK>
-constexpr int kTraceMinBlocks = BACK ? 4 : 6;
+// Walker block shape (BX x BY warp tiles) and the blocks per SM it is compiled
+// for (register cap 65536 / (32 BX BY MINB)): the forward walk is fastest at
+// 2x2 tiles, 6 blocks (80 registers, a few loop-invariant spills, 24 warps/SM),
+// the backward walk at 2x2, 4 blocks (128 registers, no spills) -- its spilled
+// values feed the RED atomics and stall them (profiles/README.md).
+#ifndef TRACE_FWD_BX
+#define TRACE_FWD_BX 2
+#define TRACE_FWD_BY 2
+#define TRACE_FWD_MINB 6
+#endif
+#ifndef TRACE_BWD_BX
+#define TRACE_BWD_BX 2
+#define TRACE_BWD_BY 2
+#define TRACE_BWD_MINB 4
+#endif
+template <bool BACK> struct TraceShape;
+template <> struct TraceShape<false> {
+    static constexpr int BX = TRACE_FWD_BX, BY = TRACE_FWD_BY, MINB = TRACE_FWD_MINB;
+};
+template <> struct TraceShape<true> {
+    static constexpr int BX = TRACE_BWD_BX, BY = TRACE_BWD_BY, MINB = TRACE_BWD_MINB;
+};
 
 template <bool BACK>
 static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entry,
                          const float* mu_int, float* proj, const float* y, double* acc,
                          unsigned long long* stats, cudaStream_t s) {
+    using S = TraceShape<BACK>;
     const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
     const int twl = tile_w_log();
     if (m.l2_window_bytes == 0) {
-        trace_kernel<BACK, kTraceMinBlocks<BACK>><<<trace_grid_w(c, twl), 128, 0, s>>>(TRACE_ARGS, twl, (int)m.nv);
+        trace_kernel<BACK, S::BX, S::BY, S::MINB><<<trace_grid_w(c, twl, S::BX, S::BY),
+                                                    32 * S::BX * S::BY, 0, s>>>(TRACE_ARGS, twl,
+                                                                                 (int)m.nv);
         return;
     }
     // L2 persistence hint for the face-tag records (per launch; the caller's
     // stream attributes are not touched): hits persist, misses stream.
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = trace_grid_w(c, twl);
-    cfg.blockDim = dim3(128);
+    cfg.gridDim = trace_grid_w(c, twl, S::BX, S::BY);
+    cfg.blockDim = dim3(32 * S::BX * S::BY);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
@@ -1144,7 +1165,8 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, trace_kernel<BACK, kTraceMinBlocks<BACK>>, TRACE_ARGS, twl, (int)m.nv);
+    cudaLaunchKernelEx(&cfg, trace_kernel<BACK, S::BX, S::BY, S::MINB>, TRACE_ARGS, twl,
+                       (int)m.nv);
 }
 
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
