@@ -276,7 +276,9 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         // 2^23 when host copies are pipelined, for a short prologue/epilogue)
         const int64_t per_angle = (int64_t)g->n_v * g->n_u;
         const int64_t max_chunk_rays = (pipe_in || pipe_out) ? (1LL << 23) : (1LL << 26);
-        const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(g->n_angles, max_chunk_rays / per_angle));
+        // and <= kUniMaxAngles angles (one walker launch per chunk)
+        const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(g->n_angles, kUniMaxAngles),
+                                                                      max_chunk_rays / per_angle));
         if (pipe_in) {   // all y chunks are queued at once; chunk k's trace waits for its copy
             CU(cs.after(s));
             for (int a0 = 0; a0 < g->n_angles; a0 += chunk) {
@@ -294,7 +296,7 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         CU(sc.alloc(&entry_scratch, entry_scratch_bytes(m->dev, chunk)));
         for (int a0 = 0; a0 < g->n_angles; a0 += chunk) {
             const int na = std::min(chunk, g->n_angles - a0);
-            LaunchChunk c{d_ang + a0, d_aux + a0, g->beam, na, g->n_v, g->n_u};
+            LaunchChunk c{d_ang + a0, ang.data() + a0, d_aux + a0, g->beam, na, g->n_v, g->n_u};
             CU(cudaMemsetAsync(entry, 0xff, sizeof(int) * per_angle * na, s));
             {
                 KernelTimer kt(m, TET_K_ENTRY, s);

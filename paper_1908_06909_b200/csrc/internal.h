@@ -83,8 +83,24 @@ enum StatSlot {
     ST_COUNT
 };
 
+// Block-uniform half of the walker's shear frame, one per angle (kernels.cu
+// make_frame_uni): cone -> q = source S (grid units); parallel -> q = (sx, sy,
+// axis variant) of the angle's direction, scale = |d|/|d_k| g.  tau bounds the
+// sign-filter error of every ray of the angle.  Passed by value as a
+// __grid_constant__ kernel parameter (kUniMaxAngles angles per launch).
+constexpr int kUniMaxAngles = 256;
+struct UniFrame {
+    double q[3];
+    double tau;
+    double scale;
+};
+struct UniFrames {
+    UniFrame f[kUniMaxAngles];
+};
+
 struct LaunchChunk {
     const AngleGeom* ang;   // device, chunk-local angles
+    const AngleGeom* host_ang;   // host copy of the same angles (uniform frames)
     const AngleAux* aux;    // device
     int beam, n_angles, nv, nu;
 };

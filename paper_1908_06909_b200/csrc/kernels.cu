@@ -21,6 +21,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "internal.h"
 
@@ -35,6 +36,19 @@ typedef __int128 i128;
 #define DBG_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
 #else
 #define DBG_CHECK(cond) do { } while (0)
+#endif
+
+// Walker compile-time knobs (A/B builds, profiles/README.md): uniform frames
+// in the backward walk; the forward walk's rare exact path as one call per
+// step (1) or one call per uncertified sign (0).
+#ifndef TRACE_BWD_UNI
+#define TRACE_BWD_UNI 0
+#endif
+#ifndef TRACE_PAR_UNI
+#define TRACE_PAR_UNI 1
+#endif
+#ifndef TRACE_EXACT_ONECALL
+#define TRACE_EXACT_ONECALL 1
 #endif
 
 // ------------------------------------------------------------ exact -----
@@ -110,6 +124,31 @@ __device__ __forceinline__ void thread_pixel(int nu, int tw_log, int& a, int& u,
     v = by * BY * th + (w / BX) * th + (lane >> tw_log);
 }
 
+// All the uncertified signs of one walker step in one call: bit k of the
+// returned code is [side(apex, slot k) < 0], exact for the k in `mask`, taken
+// from `neg` otherwise (one call per step keeps the caller-saved register
+// traffic of the rare path to one save/restore).
+template <int BX, int BY>
+__device__ __noinline__ unsigned exact_neg_here(const int4* __restrict__ vtx,
+                                                const AngleGeom* __restrict__ ang, int beam,
+                                                int nu, int tw_log, unsigned mask, unsigned neg,
+                                                int iap, int id0, int id1, int id2) {
+    int a, u, v;
+    thread_pixel<BX, BY>(nu, tw_log, a, u, v);
+    const RayPts r = ray_points(ang[a], beam, u, v);
+    const int4 A = __ldg(vtx + iap);
+    const int ids[3] = {id0, id1, id2};
+    for (int k = 0; k < 3; ++k) {
+        if (!(mask >> k & 1u)) continue;
+        const int4 B = __ldg(vtx + ids[k]);
+        const int sg = sos_side(A.x, A.y, A.z, B.x, B.y, B.z, r.ox, r.oy, r.oz, r.px, r.py, r.pz);
+        neg = (neg & ~(1u << k)) | (sg < 0 ? 1u << k : 0u);
+    }
+    return neg;
+}
+
+// One uncertified sign (the backward walk calls this per sign: the wider
+// exact_neg_here call makes it spill the RED weight in the loop).
 template <int BX, int BY>
 __device__ __noinline__ int exact_side_here(const int4* __restrict__ vtx,
                                             const AngleGeom* __restrict__ ang, int beam, int nu,
@@ -262,6 +301,50 @@ __device__ __forceinline__ void xform_ax(const Frame& F, const int4 v, double& x
         z = (AX & 1) ? -zz : zz;
         x = fma(-F.sx, z, (double)pick4<A::K1>(v) - F.c1);
         y = fma(-F.sy, z, (double)pick4<A::K2>(v) - F.c2);
+    }
+}
+
+// Block-uniform half of the frame (one per angle, a __grid_constant__ kernel
+// parameter indexed by blockIdx.y, so it lives in uniform registers and costs
+// the walk loop no per-thread registers -- the per-ray frame spilled at the
+// forward's 80-register cap):
+//   cone (UNI = 1): the frame origin is the source S, shared by every ray of
+//     the angle: z' = sigma (X_k - S_k), x' = (X_k1 - S_k1) - sx z' (y' alike);
+//     per ray only sx, sy.  X - S is exact in fp64, so x' has one rounding.
+//   parallel (UNI = 2): every ray has direction d: sx, sy, scale uniform;
+//     per ray only c1, c2 (z' absolute as in the generic frame).
+// tau is uniform: the host bounds (|o| + rmax) over the angle's rays and
+// (1 + |sx| + |sy|)/2 <= 2.5 (the block vote admits |D_k1|, |D_k2| <= 2 |D_k|).
+template <int AX, int UNI>
+__device__ __forceinline__ void make_frame_uni(const RayPts& r, const UniFrame& U, Frame& F) {
+    using A = Axis<AX>;
+    if constexpr (UNI == 1) {
+        const long long Dx = r.px - r.ox, Dy = r.py - r.oy, Dz = r.pz - r.oz;
+        const double adk = fabs((double)pick<A::k>(Dx, Dy, Dz));
+        F.sx = (double)pick<A::K1>(Dx, Dy, Dz) / adk;
+        F.sy = (double)pick<A::K2>(Dx, Dy, Dz) / adk;
+    } else {
+        const double o3 = (double)pick<A::k>(r.ox, r.oy, r.oz);
+        const double so3 = (AX & 1) ? -o3 : o3;
+        F.c1 = fma(-U.q[0], so3, (double)pick<A::K1>(r.ox, r.oy, r.oz));
+        F.c2 = fma(-U.q[1], so3, (double)pick<A::K2>(r.ox, r.oy, r.oz));
+    }
+}
+
+template <int AX, int UNI>
+__device__ __forceinline__ void xform_uni(const Frame& F, const UniFrame& U, const int4 v,
+                                          double& x, double& y, double& z) {
+    using A = Axis<AX>;
+    if constexpr (UNI == 1) {
+        const double zz = (double)pick4<A::k>(v) - U.q[A::k];
+        z = (AX & 1) ? -zz : zz;
+        x = fma(-F.sx, z, (double)pick4<A::K1>(v) - U.q[A::K1]);
+        y = fma(-F.sy, z, (double)pick4<A::K2>(v) - U.q[A::K2]);
+    } else {
+        const double zz = (double)pick4<A::k>(v);
+        z = (AX & 1) ? -zz : zz;
+        x = fma(-U.q[0], z, (double)pick4<A::K1>(v) - F.c1);
+        y = fma(-U.q[1], z, (double)pick4<A::K2>(v) - F.c2);
     }
 }
 
@@ -654,6 +737,21 @@ __device__ __forceinline__ bool any_abs_le(double a, double b, double c, double 
 }
 
 
+template <int AX, int UNI>
+__device__ __forceinline__ void xf(const Frame& F, const UniFrame& U, const int4 v, double& x,
+                                   double& y, double& z) {
+    if constexpr (UNI == 0) xform_ax<AX>(F, v, x, y, z);
+    else xform_uni<AX, UNI>(F, U, v, x, y, z);
+}
+
+// |D| / |D_k| * g (chord per unit of z')
+template <int UNI>
+__device__ __forceinline__ double ray_scale(const Frame& F, const UniFrame& U, double g) {
+    if constexpr (UNI == 0) return F.scale;
+    else if constexpr (UNI == 1) return sqrt(fma(F.sx, F.sx, fma(F.sy, F.sy, 1.0))) * g;
+    else return U.scale;
+}
+
 // One thread per ray, 8x4-pixel warp tiles (16x8 per block).
 // State: the entry face in three fixed slots k = 0,1,2 in cyclic order (shear
 // coordinates x', y', z' and vertex id), the apex id `iap` (from the previous
@@ -663,8 +761,8 @@ __device__ __forceinline__ bool any_abs_le(double a, double b, double c, double 
 // face, the rank of the dropped slot's vertex id among t's four ids gives the
 // position of its tag, and the tag gives the next tet and its apex
 // (DESIGN.md §5).
-template <bool BACK, int AX, int BX, int BY>
-__device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int4* __restrict__ tnode,
+template <bool BACK, int AX, int UNI, int BX, int BY>
+__device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restrict__ rec, const int4* __restrict__ tnode,
                                          const int4* __restrict__ vtx,
                                          const AngleGeom* __restrict__ ang, int beam, int a, int u,
                                          int v, int nu, int tw_log, double rmax, double g,
@@ -675,10 +773,12 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
                                          unsigned& n_lost, unsigned& n_stuck) {
         const RayPts r = ray_points(ang[a], beam, u, v);
         Frame F;
-        make_frame_ax<AX>(r, rmax, g, F);
+        if constexpr (UNI == 0) make_frame_ax<AX>(r, rmax, g, F);
+        else make_frame_uni<AX, UNI>(r, U, F);
         // chord = (z'_out - z'_in) * scale; scale is folded into y (back) or
         // applied once to the ray sum (forward)
-        const double wy = BACK ? (double)y[rid] * F.scale : 0.0;
+        const double wy = BACK ? (double)y[rid] * ray_scale<UNI>(F, U, g) : 0.0;
+        const double tau = UNI ? U.tau : F.tau;
         const int t0 = e >> 2, kin = e & 3;
         int t = t0;
         DBG_CHECK(t >= 0 && t < max_steps);
@@ -693,9 +793,9 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
         else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; }
         int iap = sel4(nodes, kin);
         double x0, y0, z0, x1, y1, z1, x2, y2, z2;
-        xform_ax<AX>(F, __ldg(vtx + id0), x0, y0, z0);
-        xform_ax<AX>(F, __ldg(vtx + id1), x1, y1, z1);
-        xform_ax<AX>(F, __ldg(vtx + id2), x2, y2, z2);
+        xf<AX, UNI>(F, U, __ldg(vtx + id0), x0, y0, z0);
+        xf<AX, UNI>(F, U, __ldg(vtx + id1), x1, y1, z1);
+        xf<AX, UNI>(F, U, __ldg(vtx + id2), x2, y2, z2);
         unsigned n_exact_init = 0;
         double zin = face_depth(x0, y0, z0, x1, y1, z1, x2, y2, z2, (z0 + z1 + z2) * (1.0 / 3.0),
                                 n_exact_init);
@@ -711,7 +811,7 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
         int4 X = __ldg(vtx + iap);                          // apex vertex (16 B)
         while (true) {
             double x3, y3, z3;
-            xform_ax<AX>(F, X, x3, y3, z3);
+            xf<AX, UNI>(F, U, X, x3, y3, z3);
             const double p0 = side2(x3, y3, x0, y0);   // side(apex, slot k)
             const double p1 = side2(x3, y3, x1, y1);
             const double p2 = side2(x3, y3, x2, y2);
@@ -726,13 +826,19 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             unsigned neg = ((unsigned)__double2hiint(p0) >> 31) |
                            (((unsigned)__double2hiint(p1) >> 30) & 2u) |
                            (((unsigned)__double2hiint(p2) >> 29) & 4u);
-            if (any_abs_le(p0, p1, p2, F.tau)) {
-                const unsigned m = neg;
-                neg = 0;
-                neg |= fabs(p0) <= F.tau ? (exact_side_here<BX, BY>(vtx, ang, beam, nu, tw_log, iap, id0) < 0 ? 1u : 0u) : (m & 1u);
-                neg |= fabs(p1) <= F.tau ? (exact_side_here<BX, BY>(vtx, ang, beam, nu, tw_log, iap, id1) < 0 ? 2u : 0u) : (m & 2u);
-                neg |= fabs(p2) <= F.tau ? (exact_side_here<BX, BY>(vtx, ang, beam, nu, tw_log, iap, id2) < 0 ? 4u : 0u) : (m & 4u);
-                n_exact += (fabs(p0) <= F.tau) + (fabs(p1) <= F.tau) + (fabs(p2) <= F.tau);
+            if (any_abs_le(p0, p1, p2, tau)) {
+                const unsigned mask = (fabs(p0) <= tau ? 1u : 0u) | (fabs(p1) <= tau ? 2u : 0u) |
+                                      (fabs(p2) <= tau ? 4u : 0u);
+                if (!BACK && TRACE_EXACT_ONECALL) {
+                    neg = exact_neg_here<BX, BY>(vtx, ang, beam, nu, tw_log, mask, neg, iap, id0, id1, id2);
+                } else {
+                    const unsigned m = neg;
+                    neg = 0;
+                    neg |= (mask & 1u) ? (exact_side_here<BX, BY>(vtx, ang, beam, nu, tw_log, iap, id0) < 0 ? 1u : 0u) : (m & 1u);
+                    neg |= (mask & 2u) ? (exact_side_here<BX, BY>(vtx, ang, beam, nu, tw_log, iap, id1) < 0 ? 2u : 0u) : (m & 2u);
+                    neg |= (mask & 4u) ? (exact_side_here<BX, BY>(vtx, ang, beam, nu, tw_log, iap, id2) < 0 ? 4u : 0u) : (m & 4u);
+                }
+                n_exact += __popc(mask);
             }
             // exit face (apex, slot i, slot i+1) for the unique i with n_i = 1,
             // n_{i+1} = 0; it drops slot j = i+2.  j by table on neg:
@@ -788,7 +894,7 @@ __device__ __forceinline__ void walk_ray(const int4* __restrict__ rec, const int
             zin = zout;
             iap = (int)hi;
         }
-        if (!BACK) sum *= F.scale;
+        if (!BACK) sum *= ray_scale<UNI>(F, U, g);
     }
 
 template <bool BACK, int BX, int BY, int MINB>
@@ -804,7 +910,8 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
                                                           const float* __restrict__ y,
                                                           double* __restrict__ acc,
                                                           unsigned long long* __restrict__ stats,
-                                                          int tw_log, int nverts) {
+                                                          int tw_log, int nverts,
+                                                          const __grid_constant__ UniFrames UF) {
     // warp tile: (1 << tw_log) x (32 >> tw_log) pixels; block = 2 x 2 warp tiles
     const int tw = 1 << tw_log, th = 32 >> tw_log;
     const int tiles_u = (nu + BX * tw - 1) / (BX * tw);
@@ -841,20 +948,42 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
             ok = (dk < 0) == (dkc < 0) && 2 * adk >= m;
         }
         if (__syncthreads_and(ok)) ax = 2 * kc + (dkc < 0 ? 1 : 0);
+        // parallel beam: the uniform shear was made for the angle's axis variant
+        if (beam != TET_BEAM_CONE && ax != (int)UF.f[a].q[2]) ax = 6;
     }
+    const UniFrame& U = UF.f[a];
     if (e >= 0) {
-#define WALK(AXV) walk_ray<BACK, AXV, BX, BY>(rec, tnode, vtx, ang, beam, a, u, v, nu, tw_log, rmax, g, \
+#define WALK(AXV, UNI) walk_ray<BACK, AXV, UNI, BX, BY>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tw_log, rmax, g, \
                                       max_steps, \
                                       nverts, e, rid, mu, y, acc, sum, n_cross, n_exact, n_lost, \
                                       n_stuck)
-        switch (ax) {
-            case 0: WALK(0); break;
-            case 1: WALK(1); break;
-            case 2: WALK(2); break;
-            case 3: WALK(3); break;
-            case 4: WALK(4); break;
-            case 5: WALK(5); break;
-            default: WALK(6); break;
+        // uniform frames in the forward walk (frees the registers it spilled);
+        // the backward walk (128 registers, no spills) keeps the per-ray frame
+        // unless TRACE_BWD_UNI (measured: slightly slower, profiles/README.md)
+        // (one kernel per beam type spills the forward walk's frame: the
+        // register allocation of this combined kernel is the measured best)
+        const bool cone = beam == TET_BEAM_CONE;
+        if (BACK && !TRACE_BWD_UNI) {
+            switch (ax) {
+                case 0: WALK(0, 0); break;
+                case 1: WALK(1, 0); break;
+                case 2: WALK(2, 0); break;
+                case 3: WALK(3, 0); break;
+                case 4: WALK(4, 0); break;
+                case 5: WALK(5, 0); break;
+                default: WALK(6, 0); break;
+            }
+        } else {
+            constexpr int PU = TRACE_PAR_UNI ? 2 : 0;
+            switch (ax) {
+                case 0: if (cone) WALK(0, 1); else WALK(0, PU); break;
+                case 1: if (cone) WALK(1, 1); else WALK(1, PU); break;
+                case 2: if (cone) WALK(2, 1); else WALK(2, PU); break;
+                case 3: if (cone) WALK(3, 1); else WALK(3, PU); break;
+                case 4: if (cone) WALK(4, 1); else WALK(4, PU); break;
+                case 5: if (cone) WALK(5, 1); else WALK(5, PU); break;
+                default: WALK(6, 0); break;
+            }
         }
 #undef WALK
     }
@@ -1137,6 +1266,53 @@ template <> struct TraceShape<true> {
     static constexpr int BX = TRACE_BWD_BX, BY = TRACE_BWD_BY, MINB = TRACE_BWD_MINB;
 };
 
+// Host half of make_frame_uni: the block-uniform frame of each angle.
+static void make_uni_frames(const DevMesh& m, const LaunchChunk& c, UniFrames& U) {
+    for (int a = 0; a < c.n_angles; ++a) {
+        const AngleGeom& G = c.host_ang[a];
+        UniFrame& f = U.f[a];
+        if (c.beam == TET_BEAM_CONE) {
+            double n2 = 0;
+            for (int i = 0; i < 3; ++i) {
+                f.q[i] = (double)G.o[i];
+                n2 += f.q[i] * f.q[i];
+            }
+            // |X - S| <= |S| + rmax;  (1 + |sx| + |sy|) / 2 <= 2.5
+            const double amax = (std::sqrt(n2) + m.rmax) * 2.5;
+            f.tau = amax * amax * 0x1p-38;
+            f.scale = 0;
+        } else {
+            // the axis variant the block vote picks for direction d (trace_kernel)
+            const long long* d = G.o;
+            const long long ax_ = std::llabs(d[0]), ay_ = std::llabs(d[1]), az_ = std::llabs(d[2]);
+            const int k = (ax_ >= ay_ && ax_ >= az_) ? 0 : (ay_ >= az_ ? 1 : 2);
+            const int AX = 2 * k + (d[k] < 0 ? 1 : 0);
+            const int c1 = (k + 1) % 3, c2 = (k + 2) % 3;
+            const int K1 = (AX & 1) ? c2 : c1, K2 = (AX & 1) ? c1 : c2;
+            const double adk = std::fabs((double)d[k]);
+            f.q[0] = (double)d[K1] / adk;
+            f.q[1] = (double)d[K2] / adk;
+            f.q[2] = (double)AX;
+            // |o| over the detector (o = P - d, convex in (u, v): corners)
+            double omax = 0;
+            for (int cv = 0; cv < 2; ++cv)
+                for (int cu = 0; cu < 2; ++cu) {
+                    const long long u = cu ? c.nu - 1 : 0, v = cv ? c.nv - 1 : 0;
+                    double n2 = 0;
+                    for (int i = 0; i < 3; ++i) {
+                        const double o = (double)(G.p00[i] + u * G.du[i] + v * G.dv[i] - d[i]);
+                        n2 += o * o;
+                    }
+                    omax = std::max(omax, std::sqrt(n2));
+                }
+            const double amax = (omax + m.rmax) * (1.0 + std::fabs(f.q[0]) + std::fabs(f.q[1])) * 0.5;
+            f.tau = amax * amax * 0x1p-38;
+            const double dx = (double)d[0], dy = (double)d[1], dz = (double)d[2];
+            f.scale = std::sqrt(dx * dx + dy * dy + dz * dz) / adk * m.g;
+        }
+    }
+}
+
 template <bool BACK>
 static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entry,
                          const float* mu_int, float* proj, const float* y, double* acc,
@@ -1144,10 +1320,12 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     using S = TraceShape<BACK>;
     const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
     const int twl = tile_w_log();
+    static thread_local UniFrames U;   // 10 KB: copied into the launch parameters
+    make_uni_frames(m, c, U);
     if (m.l2_window_bytes == 0) {
         trace_kernel<BACK, S::BX, S::BY, S::MINB><<<trace_grid_w(c, twl, S::BX, S::BY),
                                                     32 * S::BX * S::BY, 0, s>>>(TRACE_ARGS, twl,
-                                                                                 (int)m.nv);
+                                                                                 (int)m.nv, U);
         return;
     }
     // L2 persistence hint for the face-tag records (per launch; the caller's
@@ -1166,12 +1344,13 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, trace_kernel<BACK, S::BX, S::BY, S::MINB>, TRACE_ARGS, twl,
-                       (int)m.nv);
+                       (int)m.nv, U);
 }
 
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
                            const float* mu_int, float* proj, unsigned long long* stats,
                            cudaStream_t s) {
+    if (c.n_angles > kUniMaxAngles) return cudaErrorInvalidValue;   // api.cu chunks by it
     launch_trace<false>(m, c, entry, mu_int, proj, nullptr, nullptr, stats, s);
     return cudaGetLastError();
 }
@@ -1179,6 +1358,7 @@ cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* en
 cudaError_t launch_backward(const DevMesh& m, const LaunchChunk& c, const int* entry,
                             const float* y, double* acc, unsigned long long* stats,
                             cudaStream_t s) {
+    if (c.n_angles > kUniMaxAngles) return cudaErrorInvalidValue;   // api.cu chunks by it
     launch_trace<true>(m, c, entry, nullptr, nullptr, y, acc, stats, s);
     return cudaGetLastError();
 }
