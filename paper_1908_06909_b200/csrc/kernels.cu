@@ -42,7 +42,10 @@ typedef __int128 i128;
 // in the backward walk; the forward walk's rare exact path as one call per
 // step (1) or one call per uncertified sign (0).
 #ifndef TRACE_BWD_UNI
-#define TRACE_BWD_UNI 0
+#define TRACE_BWD_UNI 1
+#endif
+#ifndef TRACE_BWD_ONECALL
+#define TRACE_BWD_ONECALL 0
 #endif
 #ifndef TRACE_PAR_UNI
 #define TRACE_PAR_UNI 1
@@ -829,7 +832,7 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
             if (any_abs_le(p0, p1, p2, tau)) {
                 const unsigned mask = (fabs(p0) <= tau ? 1u : 0u) | (fabs(p1) <= tau ? 2u : 0u) |
                                       (fabs(p2) <= tau ? 4u : 0u);
-                if (!BACK && TRACE_EXACT_ONECALL) {
+                if (BACK ? TRACE_BWD_ONECALL : TRACE_EXACT_ONECALL) {
                     neg = exact_neg_here<BX, BY>(vtx, ang, beam, nu, tw_log, mask, neg, iap, id0, id1, id2);
                 } else {
                     const unsigned m = neg;
@@ -957,9 +960,7 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
                                       max_steps, \
                                       nverts, e, rid, mu, y, acc, sum, n_cross, n_exact, n_lost, \
                                       n_stuck)
-        // uniform frames in the forward walk (frees the registers it spilled);
-        // the backward walk (128 registers, no spills) keeps the per-ray frame
-        // unless TRACE_BWD_UNI (measured: slightly slower, profiles/README.md)
+        // uniform frames (TRACE_BWD_UNI = 0: per-ray frame in the backward walk)
         // (one kernel per beam type spills the forward walk's frame: the
         // register allocation of this combined kernel is the measured best)
         const bool cone = beam == TET_BEAM_CONE;
@@ -1244,10 +1245,11 @@ static dim3 trace_grid_w(const LaunchChunk& c, int tw_log, int bx, int by) {
                    mu_int, proj, y, acc, stats
 
 // Walker block shape (BX x BY warp tiles) and the blocks per SM it is compiled
-// for (register cap 65536 / (32 BX BY MINB)): the forward walk is fastest at
-// 2x2 tiles, 6 blocks (80 registers, a few loop-invariant spills, 24 warps/SM),
-// the backward walk at 2x2, 4 blocks (128 registers, no spills) -- its spilled
-// values feed the RED atomics and stall them (profiles/README.md).
+// for (register cap 65536 / (32 BX BY MINB)): with the block-uniform frame the
+// forward walk is fastest at 2x2 tiles, 6 blocks (80 registers, no spills in
+// the loop, 24 warps/SM), the backward walk at 2x2, 8 blocks (64 registers,
+// 32 warps/SM: its REDs want latency hiding more than registers)
+// (profiles/README.md).
 #ifndef TRACE_FWD_BX
 #define TRACE_FWD_BX 2
 #define TRACE_FWD_BY 2
@@ -1256,7 +1258,7 @@ static dim3 trace_grid_w(const LaunchChunk& c, int tw_log, int bx, int by) {
 #ifndef TRACE_BWD_BX
 #define TRACE_BWD_BX 2
 #define TRACE_BWD_BY 2
-#define TRACE_BWD_MINB 4
+#define TRACE_BWD_MINB 8
 #endif
 template <bool BACK> struct TraceShape;
 template <> struct TraceShape<false> {
