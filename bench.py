@@ -81,8 +81,9 @@ class ClockSampler:
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []      # (monotonic time, fields)
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
@@ -92,13 +93,27 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the sampler is live before the timed region starts
+            deadline = time.monotonic() + 5.0
+            while not self.rows and time.monotonic() < deadline:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.t0 = time.monotonic()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.monotonic(), [x.strip() for x in line.split(",")]))
+
+    def stop(self):
+        """End of the timed region: wait for the sample that covers it (a
+        region shorter than the 50-ms period still gets one)."""
+        self.t1 = time.monotonic()
+        deadline = self.t1 + 1.0
+        while self.proc and time.monotonic() < deadline and \
+                not any(t >= self.t1 for t, _ in self.rows):
+            time.sleep(0.01)
 
     def __exit__(self, *a):
         if self.proc:
@@ -109,15 +124,20 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        t1 = self.t1 if self.t1 is not None else time.monotonic()
+        # samples inside the timed region, plus the one that closes it
+        inside = [r for t, r in self.rows if self.t0 <= t <= t1]
+        after = [r for t, r in self.rows if t > t1][:1]
+        rows = inside + after
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v == "Active"})
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(rows), "samples_inside": len(inside)}
 
 
 def measured_peaks():
@@ -288,6 +308,7 @@ def main():
             backward()
             ev[i][2].record(stream)
         torch.cuda.synchronize()
+        clocks.stop()
         if ws > 1:
             dist.barrier()
     T.tet_set_kernel_timing(h, False)
