@@ -723,6 +723,19 @@ __global__ void __launch_bounds__(128) entry_bvh_kernel(const int4* __restrict__
 }
 
 // ------------------------------------------------------------ walker ----
+// #{ids < x} for four distinct ids in [0, 2^31) (one of them may be x):
+// [a < x] is the sign bit of a - x.  PTX, so that nvcc does not turn it back
+// into compare + predicated-move chains.
+__device__ __forceinline__ int rank4(int a, int b, int c, int d, int x) {
+    int r;
+    asm("{\n\t.reg .u32 p, q, s, t;\n\t"
+        "sub.u32 p, %1, %5;\n\tsub.u32 q, %2, %5;\n\tsub.u32 s, %3, %5;\n\tsub.u32 t, %4, %5;\n\t"
+        "shr.u32 p, p, 31;\n\tshr.u32 q, q, 31;\n\tshr.u32 s, s, 31;\n\tshr.u32 t, t, 31;\n\t"
+        "add.u32 p, p, q;\n\tadd.u32 s, s, t;\n\tadd.u32 %0, p, s;\n\t}"
+        : "=r"(r) : "r"(a), "r"(b), "r"(c), "r"(d), "r"(x));
+    return r;
+}
+
 // j (dropped slot) per sign code neg = n0 | n1<<1 | n2<<2, 2 bits each; 3 = lost
 constexpr unsigned kExitLUT = 3u | 2u << 2 | 0u << 4 | 0u << 6 | 1u << 8 | 2u << 10 | 1u << 12 |
                               3u << 14;
@@ -851,7 +864,9 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
             // the rank of the dropped slot's vertex
             // id among t's four vertex ids (three slots + apex), mesh_host.cpp
             const int idj = selp(id0, selp(id1, id2, j == 1), j == 0);
-            const int L = (id0 < idj) + (id1 < idj) + (id2 < idj) + (iap < idj);
+            // ids are distinct and in [0, 2^31): [a < b] is the sign bit of a - b
+            // (shift-adds, LEA.HI, instead of compare + predicated-move chains)
+            const int L = rank4(id0, id1, id2, iap, idj);
             const int lo = selp(selp(ta.x, ta.z, L == 0), selp(tb.x, tb.z, L == 2), L < 2);
             const unsigned hi = (unsigned)selp(selp(ta.y, ta.w, L == 0), selp(tb.y, tb.w, L == 2), L < 2);
             const bool more = lo >= 0 && j != 3 && ++steps != max_steps;
