@@ -90,6 +90,26 @@ def test_wide_cone_generic_frame():
     U.check_parity(m, geom, mu, y)
 
 
+@pytest.mark.parametrize("beam", ["cone", "parallel"])
+def test_many_angles_uniform_frame_chunks(beam):
+    """300 angles on a small detector: the walk launches split at 256 angles
+    (one block-uniform frame per angle in the launch parameters), and every
+    angle's frame -- cone source / parallel shear, per-angle tau -- must give
+    the oracle's crossings and values.  Angles are off the axes, so the
+    blocks run the fixed-axis variants on the uniform frame."""
+    m = M.ball_mesh(h=0.25, seed=3)
+    ang = G.equidistant(300) + 0.013
+    if beam == "cone":
+        geom = G.circular_cone(ang, 3.0, 6.0, 13, 9, 0.4, 0.4, off_u=0.11, off_v=-0.07)
+    else:
+        geom = G.circular_parallel(ang, 13, 9, 0.19, 0.2, off_u=0.05, off_v=0.03)
+    rng = np.random.default_rng(7)
+    mu = rng.uniform(0.2, 1.0, m.n_tets).astype(np.float32)
+    y = rng.uniform(0.5, 1.5, geom.n_rays).astype(np.float32)
+    r = U.check_parity(m, geom, mu, y)
+    assert r["stats"]["rays_hit"] > geom.n_rays // 4
+
+
 @pytest.mark.parametrize("case", ["c1", "lattice", "c2"])
 def test_bvh_entry_finder_identical(case):
     """NEXT-3: the per-ray BVH entry finder takes the same exact decisions as
