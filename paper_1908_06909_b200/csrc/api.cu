@@ -146,6 +146,37 @@ struct KernelTimer {
     }
 };
 
+// Second walk stream of one call: consecutive angle chunks alternate between
+// the caller's stream and this one (with their own entry buffers), so chunk
+// k+1's entry finder and the head of its walk overlap the tail of chunk k's
+// walk -- a serialised chunk boundary cost ~0.2 ms (c3, profiles/README.md).
+struct AuxStream {
+    cudaStream_t main, s = nullptr;
+    cudaError_t err = cudaSuccess;
+    static cudaError_t wait(cudaStream_t waiter, cudaStream_t on) {
+        cudaEvent_t e;
+        cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        if (r != cudaSuccess) return r;
+        r = cudaEventRecord(e, on);
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(waiter, e, 0);
+        cudaEventDestroy(e);   // released once the recorded work completes
+        return r;
+    }
+    // `on`: everything queued on the caller's stream so far is visible to it
+    AuxStream(cudaStream_t m, bool on) : main(m) {
+        if (!on) return;
+        err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        if (err == cudaSuccess) err = wait(s, main);
+    }
+    cudaStream_t get(size_t k) const { return (s && (k & 1)) ? s : main; }
+    cudaError_t join() const { return s ? wait(main, s) : cudaSuccess; }
+    ~AuxStream() {   // the caller's stream (and the scratch frees on it) waits for it
+        if (!s) return;
+        wait(main, s);
+        cudaStreamDestroy(s);
+    }
+};
+
 // Side stream for the pipelined host copies of one call, with its events.
 struct CopyStream {
     cudaStream_t s = nullptr;
@@ -275,7 +306,12 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         // --- angle chunks bound the entry-map scratch (<= 2^26 rays per chunk;
         // 2^23 when host copies are pipelined, for a short prologue/epilogue)
         const int64_t per_angle = (int64_t)g->n_v * g->n_u;
-        const int64_t max_chunk_rays = (pipe_in || pipe_out) ? (1LL << 23) : (1LL << 26);
+        static const int pipe_log = [] {   // A/B knob for the host-buffer pipeline
+            const char* e = getenv("TETPROJ_PIPE_CHUNK_LOG");
+            const int v = e ? atoi(e) : 23;
+            return v >= 16 && v <= 26 ? v : 23;
+        }();
+        const int64_t max_chunk_rays = (pipe_in || pipe_out) ? (1LL << pipe_log) : (1LL << 26);
         // and <= kUniMaxAngles angles (one walker launch per chunk)
         const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(g->n_angles, kUniMaxAngles),
                                                                       max_chunk_rays / per_angle));
@@ -290,44 +326,55 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
             }
         }
         size_t chunk_idx = 0;
-        int* entry;
-        CU(sc.alloc((void**)&entry, sizeof(int) * per_angle * chunk));
-        void* entry_scratch;
-        CU(sc.alloc(&entry_scratch, entry_scratch_bytes(m->dev, chunk)));
+        const int n_chunks = (g->n_angles + chunk - 1) / chunk;
+        const int nbuf = n_chunks > 1 ? 2 : 1;
+        int* entry[2] = {nullptr, nullptr};
+        void* entry_scratch[2] = {nullptr, nullptr};
+        for (int b = 0; b < nbuf; ++b) {
+            CU(sc.alloc((void**)&entry[b], sizeof(int) * per_angle * chunk));
+            CU(sc.alloc(&entry_scratch[b], entry_scratch_bytes(m->dev, chunk)));
+        }
+        // chunk k runs on ws.get(k) with entry buffer k % 2 (the chunk k-2
+        // that used it before is earlier on the same stream)
+        AuxStream ws(s, n_chunks > 1);
+        if (ws.err != cudaSuccess) return cuda_fail(ws.err, "walk stream");
         for (int a0 = 0; a0 < g->n_angles; a0 += chunk) {
             const int na = std::min(chunk, g->n_angles - a0);
+            cudaStream_t sk = ws.get(chunk_idx);
+            int* ent = entry[chunk_idx % nbuf];
             LaunchChunk c{d_ang + a0, ang.data() + a0, d_aux + a0, g->beam, na, g->n_v, g->n_u};
-            CU(cudaMemsetAsync(entry, 0xff, sizeof(int) * per_angle * na, s));
+            CU(cudaMemsetAsync(ent, 0xff, sizeof(int) * per_angle * na, sk));
             {
-                KernelTimer kt(m, TET_K_ENTRY, s);
+                KernelTimer kt(m, TET_K_ENTRY, sk);
                 if (entry_mode == TET_ENTRY_BVH)
-                    CU(launch_entry_bvh(m->dev, c, entry, d_stats, s));
+                    CU(launch_entry_bvh(m->dev, c, ent, d_stats, sk));
                 else
-                    CU(launch_entry(m->dev, c, entry, entry_scratch, d_stats, s));
+                    CU(launch_entry(m->dev, c, ent, entry_scratch[chunk_idx % nbuf], d_stats, sk));
             }
             const size_t off = (size_t)a0 * per_angle;
             const bool fwd = op == Op::Forward;
-            if (pipe_in) CU(cudaStreamWaitEvent(s, cs.ev[chunk_idx], 0));
+            if (pipe_in) CU(cudaStreamWaitEvent(sk, cs.ev[chunk_idx], 0));
             ++chunk_idx;
             if (mode != TET_TRAVERSE_EXACT) {
-                KernelTimer kt(m, fwd ? TET_K_FORWARD : TET_K_BACKWARD, s);
-                CU(launch_mt(m->dev, c, !fwd, mode == TET_TRAVERSE_MT_F32, mto, entry, mu_int,
+                KernelTimer kt(m, fwd ? TET_K_FORWARD : TET_K_BACKWARD, sk);
+                CU(launch_mt(m->dev, c, !fwd, mode == TET_TRAVERSE_MT_F32, mto, ent, mu_int,
                              fwd ? (float*)d_out + off : nullptr, fwd ? nullptr : d_in + off, acc,
-                             d_stats, s));
+                             d_stats, sk));
             } else if (fwd) {
-                KernelTimer kt(m, TET_K_FORWARD, s);
-                CU(launch_forward(m->dev, c, entry, mu_int, (float*)d_out + off, d_stats, s));
+                KernelTimer kt(m, TET_K_FORWARD, sk);
+                CU(launch_forward(m->dev, c, ent, mu_int, (float*)d_out + off, d_stats, sk));
             } else {
-                KernelTimer kt(m, TET_K_BACKWARD, s);
-                CU(launch_backward(m->dev, c, entry, d_in + off, acc, d_stats, s));
+                KernelTimer kt(m, TET_K_BACKWARD, sk);
+                CU(launch_backward(m->dev, c, ent, d_in + off, acc, d_stats, sk));
             }
             if (pipe_out) {   // this chunk's projections go home while the next one traces
-                CU(cs.after(s));
+                CU(cs.after(sk));
                 CU(cudaMemcpyAsync((float*)out + off, (float*)d_out + off,
                                    (size_t)na * per_angle * sizeof(float), cudaMemcpyDeviceToHost,
                                    cs.s));
             }
         }
+        CU(ws.join());
         if (pipe_out) CU(cs.join(s));
         if (op == Op::Backward) {
             KernelTimer kt(m, TET_K_PERMUTE, s);
