@@ -414,10 +414,13 @@ def main():
                          "traffic": ncu_traffic(dom, cross_unit / max(launches // args.steps, 1))
                          if args.config == "c3" else None,
                          "per_launch_ms": per_launch_b if dom == "backward" else per_launch_f,
-                         "note": "compulsory bytes per crossing (SURVEY 8(d)) x crossings / "
-                                 "walk-kernel time; the c3 working set is L2-resident, so DRAM "
-                                 "traffic is ~0.15 B/crossing and the walk is latency/issue-bound "
-                                 "(DESIGN.md 5, Roofline)",
+                         "note": "compulsory bytes per crossing (SURVEY 8(d)) x crossings per "
+                                 "step / busy time of the walk-kernel class per step (union of its "
+                                 "launch intervals, CUDA events on the launching streams: angle "
+                                 "chunks alternate between two streams and may overlap); "
+                                 "per_launch_ms = busy time / launches.  The c3 working set is "
+                                 "L2-resident (DRAM traffic ~0.2 B/crossing): the walk is "
+                                 "latency/issue-bound (DESIGN.md 5, Roofline)",
                          "gathered_bytes_per_crossing": bytes_unit,
                          "gathered_achieved": achieved,
                          "gathered_frac": achieved / peak,

@@ -174,9 +174,11 @@ tet_status tet_mesh_info(tet_mesh_t m, int64_t info[8]);
 /* Kernel timing for benchmarks / profiling.  When enabled, every call records
  * CUDA events around each of its kernel launches on the call's stream (no
  * synchronisation is added).  tet_kernel_times() -- only after that stream
- * has been synchronised -- returns the accumulated milliseconds and launch
- * counts per kernel class [0 entry finder, 1 forward walk, 2 backward walk,
- * 3 permutes] and resets them.                                             */
+ * has been synchronised -- returns per kernel class [0 entry finder,
+ * 1 forward walk, 2 backward walk, 3 permutes] the milliseconds during which
+ * at least one launch of the class was running (the union of the launch
+ * intervals: a call's angle chunks alternate between two streams and their
+ * launches may overlap) and the launch counts, and resets them.             */
 enum { TET_K_ENTRY = 0, TET_K_FORWARD = 1, TET_K_BACKWARD = 2, TET_K_PERMUTE = 3, TET_K_COUNT = 4 };
 tet_status tet_set_kernel_timing(tet_mesh_t m, int enable);
 tet_status tet_kernel_times(tet_mesh_t m, double ms[4], int64_t launches[4]);

@@ -548,16 +548,39 @@ tet_status tet_kernel_times(tet_mesh_t m, double ms[4], int64_t launches[4]) {
     if (!m || !ms || !launches) return fail(TET_E_ARG, "null argument");
     DeviceGuard guard(m->device);
     std::lock_guard<std::mutex> g(m->tmu);
+    // busy time of each class = length of the UNION of its launch intervals:
+    // a call's angle chunks run on two streams and may overlap (AuxStream)
+    std::vector<std::pair<float, float>> iv[TET_K_COUNT];
     for (auto& r : m->pending) {
-        float t = 0;
-        cudaError_t e = cudaEventElapsedTime(&t, r.a, r.b);
+        float t0 = 0, t1 = 0;
+        cudaError_t e = cudaEventElapsedTime(&t0, m->pending.front().a, r.a);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t1, m->pending.front().a, r.b);
         if (e != cudaSuccess) return cuda_fail(e, "tet_kernel_times (stream not synchronised?)");
-        m->ms[r.kind] += t;
+        iv[r.kind].push_back({t0, t1});
         m->launches[r.kind] += 1;
+    }
+    for (auto& r : m->pending) {
         m->spare.push_back(r.a);
         m->spare.push_back(r.b);
     }
     m->pending.clear();
+    for (int k = 0; k < TET_K_COUNT; ++k) {
+        std::sort(iv[k].begin(), iv[k].end());
+        double busy = 0, lo = 0, hi = 0;
+        bool open = false;
+        for (auto& x : iv[k]) {
+            if (open && x.first <= hi) {
+                hi = std::max(hi, (double)x.second);
+                continue;
+            }
+            if (open) busy += hi - lo;
+            lo = x.first;
+            hi = x.second;
+            open = true;
+        }
+        if (open) busy += hi - lo;
+        m->ms[k] += busy;
+    }
     for (int k = 0; k < TET_K_COUNT; ++k) {
         ms[k] = m->ms[k];
         launches[k] = m->launches[k];

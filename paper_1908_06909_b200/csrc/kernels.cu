@@ -44,6 +44,12 @@ typedef __int128 i128;
 #ifndef TRACE_BWD_UNI
 #define TRACE_BWD_UNI 1
 #endif
+#ifndef TRACE_BWD_WY32
+#define TRACE_BWD_WY32 1
+#endif
+#ifndef TRACE_BWD_VTX_SPLIT
+#define TRACE_BWD_VTX_SPLIT 0
+#endif
 #ifndef TRACE_BWD_ONECALL
 #define TRACE_BWD_ONECALL 0
 #endif
@@ -723,6 +729,30 @@ __global__ void __launch_bounds__(128) entry_bvh_kernel(const int4* __restrict__
 }
 
 // ------------------------------------------------------------ walker ----
+// float -> double at the point of use (volatile: nvcc would hoist a plain
+// conversion of the loop-invariant weight out of the loop and keep -- at 64
+// registers: spill -- the double)
+__device__ __forceinline__ double f2d_here(float x) {
+    double r;
+    asm volatile("cvt.f64.f32 %0, %1;" : "=d"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ double f2d_here(double x) { return x; }
+
+// Apex vertex gather.  Backward walk (64 registers): x, y and z as a 64-bit
+// and a 32-bit load when TRACE_BWD_VTX_SPLIT -- the 128-bit load's register
+// quad collided with the loop-carried tet id and nvcc copied a component out
+// of it right after the load, stalling on it (ncu source view).
+template <bool BACK>
+__device__ __forceinline__ int4 ldg_vtx(const int4* p) {
+    if (BACK && TRACE_BWD_VTX_SPLIT) {
+        const int2 xy = __ldg(reinterpret_cast<const int2*>(p));
+        const int z = __ldg(reinterpret_cast<const int*>(p) + 2);
+        return make_int4(xy.x, xy.y, z, 0);
+    }
+    return __ldg(p);
+}
+
 // #{ids < x} for four distinct ids in [0, 2^31) (one of them may be x):
 // [a < x] is the sign bit of a - x.  PTX, so that nvcc does not turn it back
 // into compare + predicated-move chains.
@@ -793,7 +823,13 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
         else make_frame_uni<AX, UNI>(r, U, F);
         // chord = (z'_out - z'_in) * scale; scale is folded into y (back) or
         // applied once to the ray sum (forward)
+#if TRACE_BWD_WY32
+        // f32 weight: one register (at 64 registers the f64 weight spilled and
+        // its local reload stalled every RED); relative error 2^-24
+        const float wy = BACK ? (float)((double)y[rid] * ray_scale<UNI>(F, U, g)) : 0.f;
+#else
         const double wy = BACK ? (double)y[rid] * ray_scale<UNI>(F, U, g) : 0.0;
+#endif
         const double tau = UNI ? U.tau : F.tau;
         const int t0 = e >> 2, kin = e & 3;
         int t = t0;
@@ -876,7 +912,7 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
                 t = lo;
                 DBG_CHECK(t >= 0 && t < max_steps && (int)hi >= 0 && (int)hi < nverts);
                 ldg_rec256(rec + 2 * (size_t)t, ta, tb);
-                X = __ldg(vtx + (int)hi);
+                X = ldg_vtx<BACK>(vtx + (int)hi);
             }
             // ---- slot update: the apex takes the dropped slot j = i+2 (cyclic
             // order is preserved); s_{i+1} <- -p_{i+1}, s_{i+2} <- p_i.  The
@@ -892,7 +928,7 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
             // may come out as -1e-16 R, which is harmless in the sum
             const double dz = zout - zin;
             if (BACK) {
-                if (dz > 0.0) atomicAdd(acc + tcur, dz * wy);
+                if (dz > 0.0) atomicAdd(acc + tcur, dz * f2d_here(wy));
             } else {
                 sum = fma(dz, (double)mut, sum);
             }
