@@ -50,6 +50,9 @@ typedef __int128 i128;
 #ifndef TRACE_BWD_VTX_SPLIT
 #define TRACE_BWD_VTX_SPLIT 0
 #endif
+#ifndef TRACE_BWD_LATE_LOADS
+#define TRACE_BWD_LATE_LOADS 1
+#endif
 #ifndef TRACE_BWD_ONECALL
 #define TRACE_BWD_ONECALL 0
 #endif
@@ -908,7 +911,13 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
             const bool more = lo >= 0 && j != 3 && ++steps != max_steps;
             const int tcur = t;
             const bool d0 = j == 0, d1 = j == 1, d2 = j == 2;
-            if (more) {
+            // backward walk: the next step's gathers are issued after this
+            // step's RED (TRACE_BWD_LATE_LOADS).  Issued here, nvcc (64
+            // registers) had to copy a component of the vertex quad out of
+            // the load's destination right away -- a stall on the load that
+            // the early issue was meant to hide (9 % of the stall samples)
+            constexpr bool late = BACK && TRACE_BWD_LATE_LOADS;
+            if (!late && more) {
                 t = lo;
                 DBG_CHECK(t >= 0 && t < max_steps && (int)hi >= 0 && (int)hi < nverts);
                 ldg_rec256(rec + 2 * (size_t)t, ta, tb);
@@ -931,6 +940,12 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
                 if (dz > 0.0) atomicAdd(acc + tcur, dz * f2d_here(wy));
             } else {
                 sum = fma(dz, (double)mut, sum);
+            }
+            if (late && more) {
+                t = lo;
+                DBG_CHECK(t >= 0 && t < max_steps && (int)hi >= 0 && (int)hi < nverts);
+                ldg_rec256(rec + 2 * (size_t)t, ta, tb);
+                X = ldg_vtx<BACK>(vtx + (int)hi);
             }
             if (!more) {
                 // hull exit (lo < 0), lost (no exit pattern; impossible with
