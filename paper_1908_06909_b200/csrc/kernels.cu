@@ -53,6 +53,9 @@ typedef __int128 i128;
 #ifndef TRACE_BWD_LATE_LOADS
 #define TRACE_BWD_LATE_LOADS 1
 #endif
+#ifndef TRACE_FWD_LATE_LOADS
+#define TRACE_FWD_LATE_LOADS 1
+#endif
 #ifndef TRACE_BWD_ONECALL
 #define TRACE_BWD_ONECALL 0
 #endif
@@ -855,10 +858,11 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
         double zin = face_depth(x0, y0, z0, x1, y1, z1, x2, y2, z2, (z0 + z1 + z2) * (1.0 / 3.0),
                                 n_exact_init);
         int steps = 0;   // crossings done before this one
-        // Software-pipelined by one step: the gathers of step k+1 (face tags of
-        // the next tet, its apex vertex, mu) are issued as soon as step k's
-        // exit face is known, and step k's chord / accumulation / slot update
-        // run while they are in flight.
+        // The gathers of step k+1 (face tags of the next tet, its apex vertex,
+        // mu) can be issued as soon as step k's exit face is known, with step
+        // k's chord / accumulation / slot update running while they are in
+        // flight (TRACE_*_LATE_LOADS = 0), or after them (= 1, the default:
+        // fewer live registers, so 8 blocks/SM without copies off the load).
         int4 ta, tb;
         ldg_rec256(rec + 2 * (size_t)t, ta, tb);             // face tags of t (32 B)
         float mut = 0.f;
@@ -911,12 +915,13 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
             const bool more = lo >= 0 && j != 3 && ++steps != max_steps;
             const int tcur = t;
             const bool d0 = j == 0, d1 = j == 1, d2 = j == 2;
-            // backward walk: the next step's gathers are issued after this
-            // step's RED (TRACE_BWD_LATE_LOADS).  Issued here, nvcc (64
+            // the next step's gathers are issued after this step's chord and
+            // accumulation (TRACE_*_LATE_LOADS).  Issued here, nvcc (64
             // registers) had to copy a component of the vertex quad out of
             // the load's destination right away -- a stall on the load that
-            // the early issue was meant to hide (9 % of the stall samples)
-            constexpr bool late = BACK && TRACE_BWD_LATE_LOADS;
+            // the early issue was meant to hide (9 % of the backward's stall
+            // samples); issued late, 32 warps/SM hide the latency instead
+            constexpr bool late = BACK ? TRACE_BWD_LATE_LOADS : TRACE_FWD_LATE_LOADS;
             if (!late && more) {
                 t = lo;
                 DBG_CHECK(t >= 0 && t < max_steps && (int)hi >= 0 && (int)hi < nverts);
@@ -1311,15 +1316,14 @@ static dim3 trace_grid_w(const LaunchChunk& c, int tw_log, int bx, int by) {
                    mu_int, proj, y, acc, stats
 
 // Walker block shape (BX x BY warp tiles) and the blocks per SM it is compiled
-// for (register cap 65536 / (32 BX BY MINB)): with the block-uniform frame the
-// forward walk is fastest at 2x2 tiles, 6 blocks (80 registers, no spills in
-// the loop, 24 warps/SM), the backward walk at 2x2, 8 blocks (64 registers,
-// 32 warps/SM: its REDs want latency hiding more than registers)
-// (profiles/README.md).
+// for (register cap 65536 / (32 BX BY MINB)): with the block-uniform frame and
+// the next step's gathers issued late (TRACE_*_LATE_LOADS) both walks are
+// fastest at 2x2 tiles, 8 blocks (64 registers, 32 warps/SM: the dependent
+// gather chain wants latency hiding more than registers; profiles/README.md).
 #ifndef TRACE_FWD_BX
 #define TRACE_FWD_BX 2
 #define TRACE_FWD_BY 2
-#define TRACE_FWD_MINB 6
+#define TRACE_FWD_MINB 8
 #endif
 #ifndef TRACE_BWD_BX
 #define TRACE_BWD_BX 2
