@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -15,6 +16,9 @@ using namespace tetproj;
 
 struct tet_mesh {
     int device = 0;
+    // walk shape hint: the last call with statistics saw > 5 % exact
+    // fallbacks per crossing (kernels.cu TraceShape<., true>)
+    std::atomic<int> exact_heavy{0};
     uint32_t flags = 0;
     HostMesh host;      // keeps grid parameters (arrays freed after upload)
     DevMesh dev;
@@ -336,6 +340,11 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         }
         // chunk k runs on ws.get(k) with entry buffer k % 2 (the chunk k-2
         // that used it before is earlier on the same stream)
+        static const int heavy_env = [] {   // TETPROJ_EXACT_HEAVY=0/1 forces the shape
+            const char* e = getenv("TETPROJ_EXACT_HEAVY");
+            return e ? atoi(e) : -1;
+        }();
+        const int heavy = heavy_env >= 0 ? (heavy_env != 0) : m->exact_heavy.load();
         AuxStream ws(s, n_chunks > 1);
         if (ws.err != cudaSuccess) return cuda_fail(ws.err, "walk stream");
         for (int a0 = 0; a0 < g->n_angles; a0 += chunk) {
@@ -343,6 +352,7 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
             cudaStream_t sk = ws.get(chunk_idx);
             int* ent = entry[chunk_idx % nbuf];
             LaunchChunk c{d_ang + a0, ang.data() + a0, d_aux + a0, g->beam, na, g->n_v, g->n_u};
+            c.exact_heavy = heavy;
             CU(cudaMemsetAsync(ent, 0xff, sizeof(int) * per_angle * na, sk));
             {
                 KernelTimer kt(m, TET_K_ENTRY, sk);
@@ -390,6 +400,8 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         CU(cudaGetLastError());
     }
     if (need_stats || !dev_out || !dev_in) CU(cudaStreamSynchronize(s));
+    if (need_stats && mode == TET_TRAVERSE_EXACT && hs[ST_CROSS] > 0)
+        m->exact_heavy.store(hs[ST_EXACT] * 20 > hs[ST_CROSS] ? 1 : 0);
     if (st) {
         std::memset(st, 0, sizeof *st);
         st->rays = (uint64_t)nrays;

@@ -103,6 +103,7 @@ struct LaunchChunk {
     const AngleGeom* host_ang;   // host copy of the same angles (uniform frames)
     const AngleAux* aux;    // device
     int beam, n_angles, nv, nu;
+    int exact_heavy = 0;     // walk shape for exact-heavy scans (kernels.cu TraceShape)
 };
 
 // kernel launchers (kernels.cu)

@@ -813,7 +813,7 @@ __device__ __forceinline__ double ray_scale(const Frame& F, const UniFrame& U, d
 // face, the rank of the dropped slot's vertex id among t's four ids gives the
 // position of its tag, and the tag gives the next tet and its apex
 // (DESIGN.md §5).
-template <bool BACK, int AX, int UNI, int BX, int BY>
+template <bool BACK, int AX, int UNI, int BX, int BY, bool LATE>
 __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restrict__ rec, const int4* __restrict__ tnode,
                                          const int4* __restrict__ vtx,
                                          const AngleGeom* __restrict__ ang, int beam, int a, int u,
@@ -921,7 +921,7 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
             // the load's destination right away -- a stall on the load that
             // the early issue was meant to hide (9 % of the backward's stall
             // samples); issued late, 32 warps/SM hide the latency instead
-            constexpr bool late = BACK ? TRACE_BWD_LATE_LOADS : TRACE_FWD_LATE_LOADS;
+            constexpr bool late = LATE;
             if (!late && more) {
                 t = lo;
                 DBG_CHECK(t >= 0 && t < max_steps && (int)hi >= 0 && (int)hi < nverts);
@@ -971,7 +971,7 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
         if (!BACK) sum *= ray_scale<UNI>(F, U, g);
     }
 
-template <bool BACK, int BX, int BY, int MINB>
+template <bool BACK, int BX, int BY, int MINB, bool LATE>
 __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* __restrict__ rec,
                                                           const int4* __restrict__ tnode,
                                                           const int4* __restrict__ vtx,
@@ -1027,7 +1027,7 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
     }
     const UniFrame& U = UF.f[a];
     if (e >= 0) {
-#define WALK(AXV, UNI) walk_ray<BACK, AXV, UNI, BX, BY>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tw_log, rmax, g, \
+#define WALK(AXV, UNI) walk_ray<BACK, AXV, UNI, BX, BY, LATE>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tw_log, rmax, g, \
                                       max_steps, \
                                       nverts, e, rid, mu, y, acc, sum, n_cross, n_exact, n_lost, \
                                       n_stuck)
@@ -1330,12 +1330,32 @@ static dim3 trace_grid_w(const LaunchChunk& c, int tw_log, int bx, int by) {
 #define TRACE_BWD_BY 2
 #define TRACE_BWD_MINB 8
 #endif
-template <bool BACK> struct TraceShape;
-template <> struct TraceShape<false> {
+// Exact-heavy scans (a large share of the signs go to the int128 + SoS
+// path, e.g. lattice rays through mesh vertices, c4a) run a second shape:
+// fewer blocks, more registers, early gathers -- at 64 registers each
+// noinline exact call saves and restores live state and the exact path
+// itself spills (c4a 7.8e9 -> 4.6e9 crossings/s with the fast shape).
+// api.cu picks it from the exact-fallback rate of the mesh's last call with
+// statistics (LaunchChunk::exact_heavy).
+template <bool BACK, bool HEAVY> struct TraceShape;
+template <> struct TraceShape<false, false> {
     static constexpr int BX = TRACE_FWD_BX, BY = TRACE_FWD_BY, MINB = TRACE_FWD_MINB;
+    static constexpr bool LATE = TRACE_FWD_LATE_LOADS;
 };
-template <> struct TraceShape<true> {
+template <> struct TraceShape<true, false> {
     static constexpr int BX = TRACE_BWD_BX, BY = TRACE_BWD_BY, MINB = TRACE_BWD_MINB;
+    static constexpr bool LATE = TRACE_BWD_LATE_LOADS;
+};
+#ifndef TRACE_HEAVY_FWD_MINB
+#define TRACE_HEAVY_FWD_MINB 4
+#endif
+template <> struct TraceShape<false, true> {
+    static constexpr int BX = 2, BY = 2, MINB = TRACE_HEAVY_FWD_MINB;
+    static constexpr bool LATE = false;
+};
+template <> struct TraceShape<true, true> {
+    static constexpr int BX = 2, BY = 2, MINB = 4;
+    static constexpr bool LATE = false;
 };
 
 // Host half of make_frame_uni: the block-uniform frame of each angle.
@@ -1385,19 +1405,19 @@ static void make_uni_frames(const DevMesh& m, const LaunchChunk& c, UniFrames& U
     }
 }
 
-template <bool BACK>
+template <bool BACK, bool HEAVY>
 static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entry,
                          const float* mu_int, float* proj, const float* y, double* acc,
                          unsigned long long* stats, cudaStream_t s) {
-    using S = TraceShape<BACK>;
+    using S = TraceShape<BACK, HEAVY>;
     const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
     const int twl = tile_w_log();
     static thread_local UniFrames U;   // 10 KB: copied into the launch parameters
     make_uni_frames(m, c, U);
     if (m.l2_window_bytes == 0) {
-        trace_kernel<BACK, S::BX, S::BY, S::MINB><<<trace_grid_w(c, twl, S::BX, S::BY),
-                                                    32 * S::BX * S::BY, 0, s>>>(TRACE_ARGS, twl,
-                                                                                 (int)m.nv, U);
+        trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE>
+            <<<trace_grid_w(c, twl, S::BX, S::BY), 32 * S::BX * S::BY, 0, s>>>(TRACE_ARGS, twl,
+                                                                               (int)m.nv, U);
         return;
     }
     // L2 persistence hint for the face-tag records (per launch; the caller's
@@ -1415,15 +1435,16 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, trace_kernel<BACK, S::BX, S::BY, S::MINB>, TRACE_ARGS, twl,
-                       (int)m.nv, U);
+    cudaLaunchKernelEx(&cfg, trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE>, TRACE_ARGS,
+                       twl, (int)m.nv, U);
 }
 
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
                            const float* mu_int, float* proj, unsigned long long* stats,
                            cudaStream_t s) {
     if (c.n_angles > kUniMaxAngles) return cudaErrorInvalidValue;   // api.cu chunks by it
-    launch_trace<false>(m, c, entry, mu_int, proj, nullptr, nullptr, stats, s);
+    if (c.exact_heavy) launch_trace<false, true>(m, c, entry, mu_int, proj, nullptr, nullptr, stats, s);
+    else launch_trace<false, false>(m, c, entry, mu_int, proj, nullptr, nullptr, stats, s);
     return cudaGetLastError();
 }
 
@@ -1431,7 +1452,8 @@ cudaError_t launch_backward(const DevMesh& m, const LaunchChunk& c, const int* e
                             const float* y, double* acc, unsigned long long* stats,
                             cudaStream_t s) {
     if (c.n_angles > kUniMaxAngles) return cudaErrorInvalidValue;   // api.cu chunks by it
-    launch_trace<true>(m, c, entry, nullptr, nullptr, y, acc, stats, s);
+    if (c.exact_heavy) launch_trace<true, true>(m, c, entry, nullptr, nullptr, y, acc, stats, s);
+    else launch_trace<true, false>(m, c, entry, nullptr, nullptr, y, acc, stats, s);
     return cudaGetLastError();
 }
 

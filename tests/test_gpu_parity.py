@@ -336,3 +336,72 @@ def test_paper_mt_modes_run_and_agree_on_generic_rays():
     x, stb = tm.backproject(w.geom, torch.from_numpy(w.y).cuda(), stats=True,
                             opts=T.options(T.TET_TRAVERSE_MT_F64))
     assert stb["crossings"] > 0
+
+
+def test_kernel_times_are_busy_time():
+    """tet_kernel_times reports the busy time of each kernel class (union of
+    launch intervals): with a call's angle chunks alternating between two
+    streams, the forward busy time never exceeds the call's own duration,
+    and both chunks' launches are counted."""
+    import torch
+
+    from paper_1908_06909_b200 import tetproj as T
+    w = CF.workload("c2", n_angles=300, n_u=40, n_v=32)      # 2 chunks (256 + 44)
+    tm = T.TetMesh.from_mesh(w.mesh)
+    mu = torch.from_numpy(w.mu).cuda()
+    proj = torch.empty((w.geom.n_angles, w.geom.n_v, w.geom.n_u), device="cuda")
+    T.tet_project(tm.handle, w.geom, mu, proj)               # warm
+    torch.cuda.synchronize()
+    T.tet_set_kernel_timing(tm.handle, True)
+    T.tet_kernel_times(tm.handle)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    T.tet_project(tm.handle, w.geom, mu, proj)
+    b.record()
+    torch.cuda.synchronize()
+    T.tet_set_kernel_timing(tm.handle, False)
+    kt = T.tet_kernel_times(tm.handle)
+    call_ms = a.elapsed_time(b)
+    ms_f, n_f = kt["forward"]
+    ms_e, n_e = kt["entry"]
+    assert n_f == 2 and n_e == 2, kt
+    assert 0 < ms_f <= call_ms * 1.001 + 0.01, (kt, call_ms)
+    assert 0 < ms_e <= call_ms * 1.001 + 0.01, (kt, call_ms)
+
+
+def test_exact_heavy_walk_shape_same_results():
+    """A call whose statistics show > 5 % exact fallbacks per crossing makes the
+    mesh's next calls run the exact-heavy walk shape (more registers, early
+    gathers).  Same arithmetic: projections bit-identical, backprojections
+    equal up to the order of the f64 atomic sums."""
+    import torch
+
+    from paper_1908_06909_b200 import tetproj as T
+    w = CF.workload("c4a", n_angles=4, n_u=64, n_v=40)
+    tm = T.TetMesh.from_mesh(w.mesh)
+    mu = torch.from_numpy(w.mu).cuda()
+    y = torch.from_numpy(w.y.reshape(-1)).cuda()
+    shape = (w.geom.n_angles, w.geom.n_v, w.geom.n_u)
+    p0 = torch.empty(shape, device="cuda")
+    x0 = torch.empty(w.mesh.n_tets, device="cuda")
+    st = T.tet_project(tm.handle, w.geom, mu, p0, stats=True)    # fast shape; learns
+    assert st["exact_fallbacks"] * 20 > st["crossings"], st
+    T.tet_backproject(tm.handle, w.geom, y, x0)                   # exact-heavy shape
+    p1 = torch.empty(shape, device="cuda")
+    T.tet_project(tm.handle, w.geom, mu, p1)                      # exact-heavy shape
+    torch.cuda.synchronize()
+    assert torch.equal(p0, p1)
+    # back to the fast shape: a call with statistics on generic rays
+    w2 = CF.workload("c2", n_angles=2, n_u=33, n_v=29)
+    tm2 = T.TetMesh.from_mesh(w2.mesh)
+    x_fast = tm2.backproject(w2.geom, torch.from_numpy(w2.y).cuda())
+    st2 = T.tet_project(tm2.handle, w2.geom, torch.from_numpy(w2.mu).cuda(),
+                        torch.empty((2, 29, 33), device="cuda"), stats=True)
+    assert st2["exact_fallbacks"] * 20 < st2["crossings"]
+    x_again = tm2.backproject(w2.geom, torch.from_numpy(w2.y).cuda())
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(x_again.cpu().numpy(), x_fast.cpu().numpy(), rtol=1e-6)
+    # and the exact-heavy backward against the oracle
+    _, xr, _, _ = U.run_oracle(w.mesh, w.geom, w.mu, w.y)
+    be = U.back_errors(x0.cpu().numpy().astype(np.float64), xr)
+    assert be.max() <= U.BACK_TOL, be.max()
