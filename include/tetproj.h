@@ -141,7 +141,10 @@ tet_status tet_mesh_destroy(tet_mesh_t m);
  *   mu   [n_tets] float, caller tet order (device or host)
  *   proj [n_angles][n_v][n_u] float (device or host), overwritten
  * st (host, nullable): if non-NULL the call synchronises cuda_stream and fills
- * it.                                                                        */
+ * it.  Performance note (results are unaffected): a call with st whose exact
+ * fallbacks exceed 5 % of its crossings switches the mesh's later calls
+ * (both directions) to a walk compiled for exact-heavy scans, and a later
+ * call with st below that rate switches back.                               */
 tet_status tet_project(tet_mesh_t m, const tet_geometry* g, const float* mu, float* proj,
                        void* cuda_stream, tet_stats* st);
 
