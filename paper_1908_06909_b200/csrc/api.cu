@@ -38,6 +38,26 @@ struct tet_mesh {
     std::vector<cudaEvent_t> spare;
     double ms[TET_K_COUNT] = {0, 0, 0, 0};
     int64_t launches[TET_K_COUNT] = {0, 0, 0, 0};
+    // side streams of the calls (second walk stream, host-copy stream),
+    // created once and reused: a cudaStreamCreate inside a timed call could
+    // stall the host while the GPU idles (seen as a ~4-ms gap in a first call)
+    std::mutex smu;
+    std::vector<cudaStream_t> streams;
+    cudaError_t take_stream(cudaStream_t& out) {
+        {
+            std::lock_guard<std::mutex> g(smu);
+            if (!streams.empty()) {
+                out = streams.back();
+                streams.pop_back();
+                return cudaSuccess;
+            }
+        }
+        return cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking);
+    }
+    void give_stream(cudaStream_t st) {   // pending work on it is fine: later use is ordered after
+        std::lock_guard<std::mutex> g(smu);
+        streams.push_back(st);
+    }
 };
 
 namespace {
@@ -155,6 +175,7 @@ struct KernelTimer {
 // k+1's entry finder and the head of its walk overlap the tail of chunk k's
 // walk -- a serialised chunk boundary cost ~0.2 ms (c3, profiles/README.md).
 struct AuxStream {
+    tet_mesh* m;
     cudaStream_t main, s = nullptr;
     cudaError_t err = cudaSuccess;
     static cudaError_t wait(cudaStream_t waiter, cudaStream_t on) {
@@ -167,27 +188,34 @@ struct AuxStream {
         return r;
     }
     // `on`: everything queued on the caller's stream so far is visible to it
-    AuxStream(cudaStream_t m, bool on) : main(m) {
+    AuxStream(tet_mesh* mesh, cudaStream_t st, bool on) : m(mesh), main(st) {
         if (!on) return;
-        err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-        if (err == cudaSuccess) err = wait(s, main);
+        err = m->take_stream(s);
+        if (err != cudaSuccess) {
+            s = nullptr;
+            return;
+        }
+        err = wait(s, main);
     }
     cudaStream_t get(size_t k) const { return (s && (k & 1)) ? s : main; }
     cudaError_t join() const { return s ? wait(main, s) : cudaSuccess; }
     ~AuxStream() {   // the caller's stream (and the scratch frees on it) waits for it
         if (!s) return;
         wait(main, s);
-        cudaStreamDestroy(s);
+        m->give_stream(s);
     }
 };
 
 // Side stream for the pipelined host copies of one call, with its events.
 struct CopyStream {
+    tet_mesh* m;
     cudaStream_t s = nullptr;
     std::vector<cudaEvent_t> ev;
     cudaError_t err = cudaSuccess;
-    explicit CopyStream(bool on) {
-        if (on) err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    CopyStream(tet_mesh* mesh, bool on) : m(mesh) {
+        if (!on) return;
+        err = m->take_stream(s);
+        if (err != cudaSuccess) s = nullptr;
     }
     cudaError_t event(cudaEvent_t& e) {
         cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -220,7 +248,7 @@ struct CopyStream {
     ~CopyStream() {   // before the scratch it reads is released (also on error paths)
         if (s) cudaStreamSynchronize(s);
         for (auto e : ev) cudaEventDestroy(e);
-        if (s) cudaStreamDestroy(s);
+        if (s) m->give_stream(s);
     }
 };
 
@@ -271,7 +299,7 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         // of the neighbouring chunks; the per-tet ones (mu, x) are small.
         const bool pipe_in = !dev_in && op != Op::Forward;
         const bool pipe_out = !dev_out && op == Op::Forward;
-        CopyStream cs(pipe_in || pipe_out);
+        CopyStream cs(m, pipe_in || pipe_out);
         if (cs.err != cudaSuccess) return cuda_fail(cs.err, "copy stream");
         const float* d_in = in;
         if (!dev_in) {
@@ -345,7 +373,7 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
             return e ? atoi(e) : -1;
         }();
         const int heavy = heavy_env >= 0 ? (heavy_env != 0) : m->exact_heavy.load();
-        AuxStream ws(s, n_chunks > 1);
+        AuxStream ws(m, s, n_chunks > 1);
         if (ws.err != cudaSuccess) return cuda_fail(ws.err, "walk stream");
         for (int a0 = 0; a0 < g->n_angles; a0 += chunk) {
             const int na = std::min(chunk, g->n_angles - a0);
@@ -512,6 +540,7 @@ tet_status tet_mesh_destroy(tet_mesh_t m) {
         cudaEventDestroy(r.b);
     }
     for (auto e : m->spare) cudaEventDestroy(e);
+    for (auto st : m->streams) cudaStreamDestroy(st);
     cudaFree(m->d_rec);
     cudaFree(m->d_tnode);
     cudaFree(m->d_vtx);

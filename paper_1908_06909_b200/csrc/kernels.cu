@@ -65,6 +65,9 @@ typedef __int128 i128;
 #ifndef ENTRY_GUIDE
 #define ENTRY_GUIDE 4u
 #endif
+#ifndef TRACE_BAND_ORDER
+#define TRACE_BAND_ORDER 1
+#endif
 #ifndef TRACE_EXACT_ONECALL
 #define TRACE_EXACT_ONECALL 1
 #endif
@@ -131,13 +134,36 @@ __device__ __noinline__ int exact_side_ids(const int4* __restrict__ vtx,
 // grid position (same mapping as trace_kernel), so (a, u, v) need not stay
 // live in registers across the walk loop.
 // Walker blocks are BX x BY warp tiles of (1 << tw_log) x (32 >> tw_log) pixels.
+// Block -> (tile column bx, tile row by, angle a) of a walk launch (grid =
+// (tiles_u x tiles_v, angles)).  TRACE_BAND_ORDER: blocks are dispatched band
+// by band -- a band is one row of tiles, roughly one z-slab of the mesh for
+// a scan about z -- with all the launch's angles of a band before the next
+// band, so the resident blocks share one slab of the mesh and its tags stay
+// in L2 across angles (c5: angle by angle, each angle streamed the whole
+// 360-MB mesh through L2, ~4 B of DRAM reads per crossing).
+__device__ __forceinline__ void block_tile(int tiles_u, bool band, int& bx, int& by, int& a) {
+    if (band) {
+        const unsigned L = blockIdx.y * gridDim.x + blockIdx.x;   // dispatch order
+        const unsigned r = L / (unsigned)tiles_u;
+        bx = (int)(L - r * (unsigned)tiles_u);
+        a = (int)(r % gridDim.y);
+        by = (int)(r / gridDim.y);
+    } else {
+        bx = blockIdx.x % tiles_u;
+        by = blockIdx.x / tiles_u;
+        a = blockIdx.y;
+    }
+}
+
+// tile_code = tw_log | band << 4 (the walk launch's tile width and block order)
 template <int BX, int BY>
-__device__ __forceinline__ void thread_pixel(int nu, int tw_log, int& a, int& u, int& v) {
+__device__ __forceinline__ void thread_pixel(int nu, int tile_code, int& a, int& u, int& v) {
+    const int tw_log = tile_code & 15;
     const int tw = 1 << tw_log, th = 32 >> tw_log;
     const int tiles_u = (nu + BX * tw - 1) / (BX * tw);
-    const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
+    int bx, by;
+    block_tile(tiles_u, (tile_code >> 4) & 1, bx, by, a);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    a = blockIdx.y;
     u = bx * BX * tw + (w % BX) * tw + (lane & (tw - 1));
     v = by * BY * th + (w / BX) * th + (lane >> tw_log);
 }
@@ -1006,11 +1032,14 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
                                                           unsigned long long* __restrict__ stats,
                                                           int tw_log, int nverts,
                                                           const __grid_constant__ UniFrames UF) {
-    // warp tile: (1 << tw_log) x (32 >> tw_log) pixels; block = 2 x 2 warp tiles
+    // warp tile: (1 << tw_log) x (32 >> tw_log) pixels; block = BX x BY warp
+    // tiles; the argument carries tw_log | band << 4 (thread_pixel)
+    const int tile_code = tw_log;
+    tw_log &= 15;
     const int tw = 1 << tw_log, th = 32 >> tw_log;
     const int tiles_u = (nu + BX * tw - 1) / (BX * tw);
-    const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
-    const int a = blockIdx.y;
+    int bx, by, a;
+    block_tile(tiles_u, (tile_code >> 4) & 1, bx, by, a);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int u = bx * BX * tw + (w % BX) * tw + (lane & (tw - 1));
     const int v = by * BY * th + (w / BX) * th + (lane >> tw_log);
@@ -1047,7 +1076,7 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
     }
     const UniFrame& U = UF.f[a];
     if (e >= 0) {
-#define WALK(AXV, UNI) walk_ray<BACK, AXV, UNI, BX, BY, LATE>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tw_log, rmax, g, \
+#define WALK(AXV, UNI) walk_ray<BACK, AXV, UNI, BX, BY, LATE>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tile_code, rmax, g, \
                                       max_steps, \
                                       nverts, e, rid, mu, y, acc, sum, n_cross, n_exact, n_lost, \
                                       n_stuck)
@@ -1325,6 +1354,16 @@ static int tile_w_log() {
     return v;
 }
 
+static size_t l2_bytes() {
+    static const size_t v = [] {
+        int dev = 0, b = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&b, cudaDevAttrL2CacheSize, dev);
+        return (size_t)(b > 0 ? b : 126 << 20);
+    }();
+    return v;
+}
+
 static dim3 trace_grid_w(const LaunchChunk& c, int tw_log, int bx, int by) {
     const int tw = 1 << tw_log, th = 32 >> tw_log;
     const unsigned tiles = (unsigned)(((c.nu + bx * tw - 1) / (bx * tw)) *
@@ -1432,11 +1471,18 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     using S = TraceShape<BACK, HEAVY>;
     const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
     const int twl = tile_w_log();
+    // band-ordered blocks (block_tile) for the forward walk of a mesh whose
+    // tag records do not fit in half the L2 (c5: 337 MB).  Not for the
+    // backward walk: rays of many angles through the same slab at once make
+    // the f64 REDs collide (c3 backward 34.8 -> 52.9 ms); nor for L2-resident
+    // meshes (c3 forward 27.1 -> 27.3 ms).
+    const int band = (!BACK && TRACE_BAND_ORDER && (size_t)m.nt * 32 > l2_bytes() / 2) ? 1 : 0;
+    const int tile_code = twl | band << 4;
     static thread_local UniFrames U;   // 10 KB: copied into the launch parameters
     make_uni_frames(m, c, U);
     if (m.l2_window_bytes == 0) {
         trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE>
-            <<<trace_grid_w(c, twl, S::BX, S::BY), 32 * S::BX * S::BY, 0, s>>>(TRACE_ARGS, twl,
+            <<<trace_grid_w(c, twl, S::BX, S::BY), 32 * S::BX * S::BY, 0, s>>>(TRACE_ARGS, tile_code,
                                                                                (int)m.nv, U);
         return;
     }
@@ -1456,7 +1502,7 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE>, TRACE_ARGS,
-                       twl, (int)m.nv, U);
+                       tile_code, (int)m.nv, U);
 }
 
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
