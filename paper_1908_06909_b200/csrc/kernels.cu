@@ -68,6 +68,9 @@ typedef __int128 i128;
 #ifndef TRACE_BAND_ORDER
 #define TRACE_BAND_ORDER 1
 #endif
+#ifndef TRACE_BWD_BAND_GROUP
+#define TRACE_BWD_BAND_GROUP 2
+#endif
 #ifndef TRACE_EXACT_ONECALL
 #define TRACE_EXACT_ONECALL 1
 #endif
@@ -141,13 +144,29 @@ __device__ __noinline__ int exact_side_ids(const int4* __restrict__ vtx,
 // band, so the resident blocks share one slab of the mesh and its tags stay
 // in L2 across angles (c5: angle by angle, each angle streamed the whole
 // 360-MB mesh through L2, ~4 B of DRAM reads per crossing).
-__device__ __forceinline__ void block_tile(int tiles_u, bool band, int& bx, int& by, int& a) {
-    if (band) {
+__device__ __forceinline__ void block_tile(int tiles_u, int group, int& bx, int& by, int& a) {
+    // group = 0: angle by angle.  group = G > 0: angles in groups of G, and
+    // within a group band by band (all G angles of a band before the next
+    // band); G >= the launch's angles is plain band order.
+    if (group > 0) {
         const unsigned L = blockIdx.y * gridDim.x + blockIdx.x;   // dispatch order
-        const unsigned r = L / (unsigned)tiles_u;
-        bx = (int)(L - r * (unsigned)tiles_u);
-        a = (int)(r % gridDim.y);
-        by = (int)(r / gridDim.y);
+        const unsigned na = gridDim.y, tiles = gridDim.x;
+        const unsigned G = min((unsigned)group, na);
+        const unsigned full = na / G;                    // complete groups
+        unsigned ag, g, Lg;
+        if (L < full * G * tiles) {
+            ag = L / (G * tiles);
+            g = G;
+            Lg = L - ag * G * tiles;
+        } else {                                         // last, partial group
+            ag = full;
+            g = na - full * G;
+            Lg = L - full * G * tiles;
+        }
+        const unsigned r = Lg / (unsigned)tiles_u;
+        bx = (int)(Lg - r * (unsigned)tiles_u);
+        a = (int)(ag * G + r % g);
+        by = (int)(r / g);
     } else {
         bx = blockIdx.x % tiles_u;
         by = blockIdx.x / tiles_u;
@@ -155,14 +174,14 @@ __device__ __forceinline__ void block_tile(int tiles_u, bool band, int& bx, int&
     }
 }
 
-// tile_code = tw_log | band << 4 (the walk launch's tile width and block order)
+// tile_code = tw_log | group << 4 (the walk launch's tile width and block order)
 template <int BX, int BY>
 __device__ __forceinline__ void thread_pixel(int nu, int tile_code, int& a, int& u, int& v) {
     const int tw_log = tile_code & 15;
     const int tw = 1 << tw_log, th = 32 >> tw_log;
     const int tiles_u = (nu + BX * tw - 1) / (BX * tw);
     int bx, by;
-    block_tile(tiles_u, (tile_code >> 4) & 1, bx, by, a);
+    block_tile(tiles_u, tile_code >> 4, bx, by, a);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     u = bx * BX * tw + (w % BX) * tw + (lane & (tw - 1));
     v = by * BY * th + (w / BX) * th + (lane >> tw_log);
@@ -1033,13 +1052,13 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
                                                           int tw_log, int nverts,
                                                           const __grid_constant__ UniFrames UF) {
     // warp tile: (1 << tw_log) x (32 >> tw_log) pixels; block = BX x BY warp
-    // tiles; the argument carries tw_log | band << 4 (thread_pixel)
+    // tiles; the argument carries tw_log | group << 4 (thread_pixel)
     const int tile_code = tw_log;
     tw_log &= 15;
     const int tw = 1 << tw_log, th = 32 >> tw_log;
     const int tiles_u = (nu + BX * tw - 1) / (BX * tw);
     int bx, by, a;
-    block_tile(tiles_u, (tile_code >> 4) & 1, bx, by, a);
+    block_tile(tiles_u, tile_code >> 4, bx, by, a);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int u = bx * BX * tw + (w % BX) * tw + (lane & (tw - 1));
     const int v = by * BY * th + (w / BX) * th + (lane >> tw_log);
@@ -1471,13 +1490,15 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     using S = TraceShape<BACK, HEAVY>;
     const int steps = (int)(m.nt < 0x7fffffff ? m.nt : 0x7fffffff);
     const int twl = tile_w_log();
-    // band-ordered blocks (block_tile) for the forward walk of a mesh whose
-    // tag records do not fit in half the L2 (c5: 337 MB).  Not for the
-    // backward walk: rays of many angles through the same slab at once make
-    // the f64 REDs collide (c3 backward 34.8 -> 52.9 ms); nor for L2-resident
-    // meshes (c3 forward 27.1 -> 27.3 ms).
-    const int band = (!BACK && TRACE_BAND_ORDER && (size_t)m.nt * 32 > l2_bytes() / 2) ? 1 : 0;
-    const int tile_code = twl | band << 4;
+    // band-ordered blocks (block_tile) for a mesh whose tag records do not
+    // fit in half the L2 (c5: 337 MB): all the launch's angles per band in
+    // the forward walk; angle pairs in the backward walk -- rays of many
+    // angles through the same slab at once make its f64 REDs collide (full
+    // band order: c3 backward 34.8 -> 52.9 ms).  L2-resident meshes keep
+    // angle order (c3 forward 27.1 -> 27.3 ms with bands).
+    const bool big = TRACE_BAND_ORDER && (size_t)m.nt * 32 > l2_bytes() / 2;
+    const int group = big ? (BACK ? TRACE_BWD_BAND_GROUP : 1 << 20) : 0;
+    const int tile_code = twl | group << 4;
     static thread_local UniFrames U;   // 10 KB: copied into the launch parameters
     make_uni_frames(m, c, U);
     if (m.l2_window_bytes == 0) {
