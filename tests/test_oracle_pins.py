@@ -4,7 +4,8 @@
 * the SoS sign table against the full delta-polynomial
 * closed forms: unit-tet chord, Kuhn cube axis integral (tests/golden/),
   box-hull slab chord, ball sandwich bounds
-* invariants: adjoint, dense-A agreement, reversal, hull-chord conservation
+* invariants: adjoint, dense-A agreement, reversal, hull-chord conservation,
+  isometry (signed axis permutations of mesh + rays)
 """
 import itertools
 import json
@@ -333,3 +334,40 @@ def test_stats_and_crossings_consistent():
     assert total == st["crossings"]
     _, st2 = O.backproject(om, w.geom, w.y)
     assert st2["crossings"] == st["crossings"]
+
+
+# signed axis permutations: (perm, signs); odd ones flip every tet's orientation
+_ISOMETRIES = [((1, 2, 0), (1, 1, 1)), ((1, 0, 2), (1, 1, 1)), ((0, 1, 2), (-1, 1, 1)),
+               ((2, 1, 0), (1, -1, -1)), ((2, 0, 1), (-1, -1, -1))]
+
+
+@pytest.mark.parametrize("perm,signs", _ISOMETRIES)
+def test_isometry_invariance(perm, signs):
+    """Eq. 1-3: a_ij is a length, so moving mesh and rays by the same
+    isometry leaves every pixel and every per-tet value unchanged.  Signed axis
+    permutations are exact on the snapping grid (SURVEY 8(b) Grid: c and r map
+    with the vertices, rint is odd), so a dropped or transposed component in
+    the predicate or the chord (which is not symmetric under these maps)
+    breaks it.  Generic rays only: SoS (8(c) reading 6) is not invariant."""
+    Q = np.zeros((3, 3))
+    for i, (j, s) in enumerate(zip(perm, signs)):
+        Q[i, j] = s
+    m = M.random_small_mesh(40, 11)
+    geom = G.circular_cone(G.equidistant(3) + 0.37, 4.0, 8.0, 13, 11, 0.37, 0.41,
+                           off_u=0.21, off_v=-0.13)
+    m2 = M.Mesh(m.name + "_iso", m.verts @ Q.T, m.tets, m.nbrs, m.bfaces)
+    v2 = geom.vecs.reshape(-1, 4, 3) @ Q.T
+    g2 = G.Geometry(geom.beam, geom.n_v, geom.n_u, np.ascontiguousarray(v2.reshape(-1, 12)))
+    rng = np.random.default_rng(12)
+    mu = rng.uniform(0.5, 1.5, m.n_tets)
+    y = rng.uniform(0.5, 1.5, geom.n_rays)
+    om, om2 = O.OracleMesh.from_mesh(m), O.OracleMesh.from_mesh(m2)
+    p1, s1 = O.project(om, geom, mu)
+    p2, s2 = O.project(om2, g2, mu)
+    x1, _ = O.backproject(om, geom, y)
+    x2, _ = O.backproject(om2, g2, y)
+    assert s1["rays_hit"] > 50 and s1["lost"] == s2["lost"] == 0
+    assert s1["crossings"] == s2["crossings"] and s1["rays_hit"] == s2["rays_hit"]
+    np.testing.assert_allclose(p2, p1, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(x2, x1, rtol=1e-12, atol=1e-12)
+    assert np.count_nonzero(x1) > m.n_tets // 2
