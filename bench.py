@@ -158,13 +158,14 @@ def l2_gather_peak():
         return None
 
 
-def ncu_traffic(kernel, crossings_per_launch):
+def ncu_traffic(config, kernel, crossings_per_launch):
     """DRAM bytes per launch of the walk kernel: ncu's dram__bytes_read.sum +
     dram__bytes_write.sum per crossing (profiles/ncu_traffic.json, from one
-    `ncu --set full` capture of this bench's c3 launches) x crossings/launch."""
+    `ncu --set full` capture of this bench's launches of `config`) x
+    crossings/launch; None for a config without a capture."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        per = json.load(open(p))[kernel]["dram_bytes_per_crossing"]
+        per = json.load(open(p))[config][kernel]["dram_bytes_per_crossing"]
         return per * crossings_per_launch
     except Exception:
         return None
@@ -411,16 +412,18 @@ def main():
                          "achieved": achieved_c, "peak": peak, "unit": "GB/s",
                          "frac": achieved_c / peak, "peak_source": peak_src,
                          "bytes_per_crossing": comp_unit,
-                         "traffic": ncu_traffic(dom, cross_unit / max(launches // args.steps, 1))
-                         if args.config == "c3" else None,
+                         "traffic": ncu_traffic(args.config, dom,
+                                                cross_unit / max(launches // args.steps, 1)),
                          "per_launch_ms": per_launch_b if dom == "backward" else per_launch_f,
                          "note": "compulsory bytes per crossing (SURVEY 8(d)) x crossings per "
                                  "step / busy time of the walk-kernel class per step (union of its "
                                  "launch intervals, CUDA events on the launching streams: angle "
                                  "chunks alternate between two streams and may overlap); "
-                                 "per_launch_ms = busy time / launches.  The c3 working set is "
-                                 "L2-resident (DRAM traffic ~0.2 B/crossing): the walk is "
-                                 "latency/issue-bound (DESIGN.md 5, Roofline)",
+                                 "per_launch_ms = busy time / launches.  ncu DRAM traffic is "
+                                 "0.2-0.3 B/crossing on c3 (L2-resident) and on c5 (band-ordered "
+                                 "dispatch keeps a mesh slab in L2 across angles), L2 hit rate "
+                                 "~96 %: the walk is L2-fed and latency/issue-bound (DESIGN.md 5, "
+                                 "Roofline); traffic = that per-crossing figure x crossings/launch",
                          "gathered_bytes_per_crossing": bytes_unit,
                          "gathered_achieved": achieved,
                          "gathered_frac": achieved / peak,
