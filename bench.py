@@ -419,10 +419,11 @@ def main():
                                  "step / busy time of the walk-kernel class per step (union of its "
                                  "launch intervals, CUDA events on the launching streams: angle "
                                  "chunks alternate between two streams and may overlap); "
-                                 "per_launch_ms = busy time / launches.  ncu DRAM traffic is "
-                                 "0.2-0.3 B/crossing on c3 (L2-resident) and on c5 (band-ordered "
-                                 "dispatch keeps a mesh slab in L2 across angles), L2 hit rate "
-                                 "~96 %: the walk is L2-fed and latency/issue-bound (DESIGN.md 5, "
+                                 "per_launch_ms = busy time / launches.  ncu DRAM traffic per "
+                                 "crossing: c3 0.27 fwd / 0.22 back (L2-resident); c5 0.30 fwd "
+                                 "(band order keeps a mesh slab in L2 across angles) / 2.9 back "
+                                 "(0.39 TB/s, 6 % of HBM) at the same crossing rate as c3: the walk "
+                                 "is latency/issue-bound, not bandwidth-bound (DESIGN.md 5, "
                                  "Roofline); traffic = that per-crossing figure x crossings/launch",
                          "gathered_bytes_per_crossing": bytes_unit,
                          "gathered_achieved": achieved,
