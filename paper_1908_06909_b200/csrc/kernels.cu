@@ -175,13 +175,23 @@ __device__ __forceinline__ void block_tile(int tiles_u, int group, int& bx, int&
 }
 
 // tile_code = tw_log | group << 4 (the walk launch's tile width and block order)
-template <int BX, int BY>
+// BAND (compile time): band-ordered launch, tile_code = tw_log | group << 4;
+// otherwise tile_code = tw_log and the mapping reads blockIdx directly (the
+// non-band kernels keep (a, bx, by) rematerialisable from blockIdx: with the
+// runtime decode, c3 lost 1.5 % forward / 2.7 % backward to extra spills).
+template <int BX, int BY, bool BAND>
 __device__ __forceinline__ void thread_pixel(int nu, int tile_code, int& a, int& u, int& v) {
-    const int tw_log = tile_code & 15;
+    const int tw_log = BAND ? (tile_code & 15) : tile_code;
     const int tw = 1 << tw_log, th = 32 >> tw_log;
     const int tiles_u = (nu + BX * tw - 1) / (BX * tw);
     int bx, by;
-    block_tile(tiles_u, tile_code >> 4, bx, by, a);
+    if (BAND) {
+        block_tile(tiles_u, tile_code >> 4, bx, by, a);
+    } else {
+        bx = blockIdx.x % tiles_u;
+        by = blockIdx.x / tiles_u;
+        a = blockIdx.y;
+    }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     u = bx * BX * tw + (w % BX) * tw + (lane & (tw - 1));
     v = by * BY * th + (w / BX) * th + (lane >> tw_log);
@@ -191,13 +201,13 @@ __device__ __forceinline__ void thread_pixel(int nu, int tile_code, int& a, int&
 // returned code is [side(apex, slot k) < 0], exact for the k in `mask`, taken
 // from `neg` otherwise (one call per step keeps the caller-saved register
 // traffic of the rare path to one save/restore).
-template <int BX, int BY>
+template <int BX, int BY, bool BAND>
 __device__ __noinline__ unsigned exact_neg_here(const int4* __restrict__ vtx,
                                                 const AngleGeom* __restrict__ ang, int beam,
                                                 int nu, int tw_log, unsigned mask, unsigned neg,
                                                 int iap, int id0, int id1, int id2) {
     int a, u, v;
-    thread_pixel<BX, BY>(nu, tw_log, a, u, v);
+    thread_pixel<BX, BY, BAND>(nu, tw_log, a, u, v);
     const RayPts r = ray_points(ang[a], beam, u, v);
     const int4 A = __ldg(vtx + iap);
     const int ids[3] = {id0, id1, id2};
@@ -212,12 +222,12 @@ __device__ __noinline__ unsigned exact_neg_here(const int4* __restrict__ vtx,
 
 // One uncertified sign (the backward walk calls this per sign: the wider
 // exact_neg_here call makes it spill the RED weight in the loop).
-template <int BX, int BY>
+template <int BX, int BY, bool BAND>
 __device__ __noinline__ int exact_side_here(const int4* __restrict__ vtx,
                                             const AngleGeom* __restrict__ ang, int beam, int nu,
                                             int tw_log, int ia, int ib) {
     int a, u, v;
-    thread_pixel<BX, BY>(nu, tw_log, a, u, v);
+    thread_pixel<BX, BY, BAND>(nu, tw_log, a, u, v);
     return exact_side_ids(vtx, ang, beam, a, u, v, ia, ib);
 }
 
@@ -878,7 +888,7 @@ __device__ __forceinline__ double ray_scale(const Frame& F, const UniFrame& U, d
 // face, the rank of the dropped slot's vertex id among t's four ids gives the
 // position of its tag, and the tag gives the next tet and its apex
 // (DESIGN.md §5).
-template <bool BACK, int AX, int UNI, int BX, int BY, bool LATE>
+template <bool BACK, int AX, int UNI, int BX, int BY, bool LATE, bool BAND>
 __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restrict__ rec, const int4* __restrict__ tnode,
                                          const int4* __restrict__ vtx,
                                          const AngleGeom* __restrict__ ang, int beam, int a, int u,
@@ -954,13 +964,13 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
                 const unsigned mask = (fabs(p0) <= tau ? 1u : 0u) | (fabs(p1) <= tau ? 2u : 0u) |
                                       (fabs(p2) <= tau ? 4u : 0u);
                 if (BACK ? TRACE_BWD_ONECALL : TRACE_EXACT_ONECALL) {
-                    neg = exact_neg_here<BX, BY>(vtx, ang, beam, nu, tw_log, mask, neg, iap, id0, id1, id2);
+                    neg = exact_neg_here<BX, BY, BAND>(vtx, ang, beam, nu, tw_log, mask, neg, iap, id0, id1, id2);
                 } else {
                     const unsigned m = neg;
                     neg = 0;
-                    neg |= (mask & 1u) ? (exact_side_here<BX, BY>(vtx, ang, beam, nu, tw_log, iap, id0) < 0 ? 1u : 0u) : (m & 1u);
-                    neg |= (mask & 2u) ? (exact_side_here<BX, BY>(vtx, ang, beam, nu, tw_log, iap, id1) < 0 ? 2u : 0u) : (m & 2u);
-                    neg |= (mask & 4u) ? (exact_side_here<BX, BY>(vtx, ang, beam, nu, tw_log, iap, id2) < 0 ? 4u : 0u) : (m & 4u);
+                    neg |= (mask & 1u) ? (exact_side_here<BX, BY, BAND>(vtx, ang, beam, nu, tw_log, iap, id0) < 0 ? 1u : 0u) : (m & 1u);
+                    neg |= (mask & 2u) ? (exact_side_here<BX, BY, BAND>(vtx, ang, beam, nu, tw_log, iap, id1) < 0 ? 2u : 0u) : (m & 2u);
+                    neg |= (mask & 4u) ? (exact_side_here<BX, BY, BAND>(vtx, ang, beam, nu, tw_log, iap, id2) < 0 ? 4u : 0u) : (m & 4u);
                 }
                 n_exact += __popc(mask);
             }
@@ -1036,7 +1046,7 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
         if (!BACK) sum *= ray_scale<UNI>(F, U, g);
     }
 
-template <bool BACK, int BX, int BY, int MINB, bool LATE>
+template <bool BACK, int BX, int BY, int MINB, bool LATE, bool BAND>
 __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* __restrict__ rec,
                                                           const int4* __restrict__ tnode,
                                                           const int4* __restrict__ vtx,
@@ -1054,11 +1064,17 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
     // warp tile: (1 << tw_log) x (32 >> tw_log) pixels; block = BX x BY warp
     // tiles; the argument carries tw_log | group << 4 (thread_pixel)
     const int tile_code = tw_log;
-    tw_log &= 15;
+    if (BAND) tw_log &= 15;
     const int tw = 1 << tw_log, th = 32 >> tw_log;
     const int tiles_u = (nu + BX * tw - 1) / (BX * tw);
     int bx, by, a;
-    block_tile(tiles_u, tile_code >> 4, bx, by, a);
+    if (BAND) {
+        block_tile(tiles_u, tile_code >> 4, bx, by, a);
+    } else {
+        bx = blockIdx.x % tiles_u;
+        by = blockIdx.x / tiles_u;
+        a = blockIdx.y;
+    }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int u = bx * BX * tw + (w % BX) * tw + (lane & (tw - 1));
     const int v = by * BY * th + (w / BX) * th + (lane >> tw_log);
@@ -1095,7 +1111,7 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
     }
     const UniFrame& U = UF.f[a];
     if (e >= 0) {
-#define WALK(AXV, UNI) walk_ray<BACK, AXV, UNI, BX, BY, LATE>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tile_code, rmax, g, \
+#define WALK(AXV, UNI) walk_ray<BACK, AXV, UNI, BX, BY, LATE, BAND>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tile_code, rmax, g, \
                                       max_steps, \
                                       nverts, e, rid, mu, y, acc, sum, n_cross, n_exact, n_lost, \
                                       n_stuck)
@@ -1501,9 +1517,10 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     const int tile_code = twl | group << 4;
     static thread_local UniFrames U;   // 10 KB: copied into the launch parameters
     make_uni_frames(m, c, U);
+    auto kern = big ? trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, true>
+                    : trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, false>;
     if (m.l2_window_bytes == 0) {
-        trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE>
-            <<<trace_grid_w(c, twl, S::BX, S::BY), 32 * S::BX * S::BY, 0, s>>>(TRACE_ARGS, tile_code,
+        kern<<<trace_grid_w(c, twl, S::BX, S::BY), 32 * S::BX * S::BY, 0, s>>>(TRACE_ARGS, tile_code,
                                                                                (int)m.nv, U);
         return;
     }
@@ -1522,7 +1539,7 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE>, TRACE_ARGS,
+    cudaLaunchKernelEx(&cfg, kern, TRACE_ARGS,
                        tile_code, (int)m.nv, U);
 }
 
