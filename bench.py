@@ -422,7 +422,7 @@ def main():
                                  "per_launch_ms = busy time / launches.  ncu DRAM traffic per "
                                  "crossing: c3 0.27 fwd / 0.22 back (L2-resident); c5 0.30 fwd "
                                  "(band order keeps a mesh slab in L2 across angles) / 2.9 back "
-                                 "(0.39 TB/s, 6 % of HBM) at the same crossing rate as c3: the walk "
+                                 "(0.39 TB/s, 6 % of HBM) within 3 % of c3's crossing rate: the walk "
                                  "is latency/issue-bound, not bandwidth-bound (DESIGN.md 5, "
                                  "Roofline); traffic = that per-crossing figure x crossings/launch",
                          "gathered_bytes_per_crossing": bytes_unit,
