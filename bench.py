@@ -3,17 +3,23 @@
 backprojection [+ all-reduce]) of the tetrahedral CT operator of
 arXiv:1908.06909 on B200, per BASELINE.json's metric.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+                  [--scaling weak|strong] [--angles A] [--impl reference]
 
 One JSON line on rank 0.  A step = tet_project(mu) + tet_backproject(y) over
-the rank's angles (weak scaling: every rank owns the same number of angles of
-an N-times-denser circular scan; the backprojection is all-reduced over NCCL).
+the rank's angles, the backprojection all-reduced over NCCL for N > 1.
+--scaling weak (default): every rank owns A angles (default: the config's)
+of an N*A-angle circular scan.  --scaling strong: the config's scan (or
+--angles total angles) is sharded over the N ranks (north_star c5: 720
+angles over 8 GPUs).  With --gpus N > 1 and no torchrun environment the
+script re-launches itself under torch.distributed.run with N local ranks.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,9 +38,10 @@ BYTES_BACK = 56  # gathered bytes per crossing, backward with f64 accumulator
 # forward; + f64 accumulator read-modify-write backward
 COMPULSORY_FWD = 24
 COMPULSORY_BACK = 36
+ISSUE_SLOTS_PER_SM = 4   # one warp instruction per SM sub-partition per cycle
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -43,8 +50,35 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--angles", type=int, default=None, help="angles per rank (default: config)")
-    return ap.parse_args()
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--angles", type=int, default=None,
+                    help="weak: angles per rank; strong: total angles (default: the config's)")
+    return ap.parse_args(argv)
+
+
+def maybe_relaunch(args) -> None:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec under
+    torch.distributed.run with one rank per local GPU.  Fails loudly when the
+    node has fewer than N GPUs (TETPROJ_DIST_BACKEND=gloo, the one-GPU logic
+    check, maps several ranks onto one device and skips that check)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return
+    if os.environ.get("TETPROJ_DIST_BACKEND", "nccl") == "nccl":
+        import torch
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, "
+                             f"this node has {n}\n")
+            sys.exit(2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def dist_env():
@@ -54,22 +88,38 @@ def dist_env():
     return ws, rank, local
 
 
-def rank_workload(cfg, rank, ws, angles_per_rank=None):
-    """Weak scaling: the full scan has ws*A equidistant angles and rank r owns
-    angles r::ws (paper_1908_06909_b200.dist.AngleSharding).  Returns the
-    workload, the FULL geometry, the rank's geometry and its detector rows."""
+def rank_workload(cfg, rank, ws, angles=None, scaling="weak"):
+    """The full scan and this rank's share (paper_1908_06909_b200.dist.
+    AngleSharding: rank r owns angles r::ws).  weak: the full scan has
+    ws * A equidistant angles (A = `angles` or the config's), so every rank
+    traces A angles; strong: the full scan has `angles` (or the config's)
+    angles, split over the ranks.  Returns the workload, the FULL geometry,
+    the rank's geometry and its detector rows."""
     from paper_1908_06909_b200.dist import AngleSharding
     from workloads import configs as CF
     w = CF.workload(cfg)
-    A = angles_per_rank or w.geom.n_angles
+    A0 = w.geom.n_angles
+    total = (angles or A0) * ws if scaling == "weak" else (angles or A0)
     if cfg in ("c2", "c3", "c4b", "c5"):
-        full = CF.workload(cfg, n_angles=A * ws).geom
-    else:
-        full = w.geom.subset(np.arange(min(A, w.geom.n_angles)))
+        full = CF.workload(cfg, n_angles=total).geom
+    else:   # fixed direction sets (c1, c4a): at most the config's angles
+        full = w.geom.subset(np.arange(min(total, A0)))
     sh = AngleSharding(full.n_angles, rank, ws)
     geom = full.subset(sh.local_angles())
     y = CF.uniform_y(geom, 1000 + rank)
     return w, full, geom, y
+
+
+def config_dict(args, w, full, geom, ws):
+    """The `config` object of both arms (same keys, so the driver can see
+    that both did the same work)."""
+    return {"workload": f"{args.config}: {w.desc}", "tets": w.mesh.n_tets,
+            "verts": w.mesh.n_verts, "hull_faces": w.mesh.n_bfaces,
+            "angles_total": full.n_angles, "angles_per_gpu": geom.n_angles,
+            "detector": [geom.n_v, geom.n_u], "beam": "cone" if geom.beam == 0 else "parallel",
+            "rays_per_step": int(full.n_rays), "parallelism": f"angles x{ws}",
+            "scaling": args.scaling,
+            "l2": "flushed between timed steps (256 MiB write, untimed)"}
 
 
 class ClockSampler:
@@ -148,14 +198,19 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def l2_gather_peak():
-    """Measured random 32-B gather rate from L2 (experiments/microbench.py,
-    profiles/r01_microbench.json): the second denominator of SURVEY §8(d)."""
+def _profile_json(name):
     try:
-        return float(json.load(open(os.path.join(ROOT, "profiles", "r01_microbench.json")))
-                     ["gather32_L2_GBps"])
+        return json.load(open(os.path.join(ROOT, "profiles", name)))
     except Exception:
         return None
+
+
+def l2_gather_peak():
+    """Measured random 32-B gather rate from L2 (experiments/microbench.py,
+    profiles/microbench.json, whose ncu capture shows it at the L2 limit):
+    the second denominator of SURVEY §8(d)."""
+    d = _profile_json("microbench.json")
+    return float(d["gather32_L2_GBps"]) if d and "gather32_L2_GBps" in d else None
 
 
 def ncu_traffic(config, kernel, crossings_per_launch):
@@ -163,19 +218,90 @@ def ncu_traffic(config, kernel, crossings_per_launch):
     dram__bytes_write.sum per crossing (profiles/ncu_traffic.json, from one
     `ncu --set full` capture of this bench's launches of `config`) x
     crossings/launch; None for a config without a capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    d = _profile_json("ncu_traffic.json")
     try:
-        per = json.load(open(p))[config][kernel]["dram_bytes_per_crossing"]
-        return per * crossings_per_launch
+        return d[config][kernel]["dram_bytes_per_crossing"] * crossings_per_launch
     except Exception:
         return None
+
+
+def ncu_issue(config, kernel):
+    """Per-crossing ncu counters of the walk kernel (profiles/ncu_issue.json:
+    smsp__inst_executed.sum / crossings of the captured launch, plus the
+    capture's issue-active, L1 data-pipe and L2 throughput percentages)."""
+    d = _profile_json("ncu_issue.json")
+    try:
+        return d[config][kernel]
+    except Exception:
+        return None
+
+
+def sm_count():
+    try:
+        import torch
+        return torch.cuda.get_device_properties(0).multi_processor_count
+    except Exception:
+        return 148
+
+
+def roofline(config, dom, cross_launch, per_launch_ms, clk_mhz):
+    """The dominant walk kernel against the limit that binds it.
+
+    The walk is a dependent gather chain served from L1/L2 (DRAM traffic
+    0.2-3 B per crossing, roofline.traffic), so neither HBM nor L2 bandwidth
+    binds; the binding resource is warp-instruction issue: `achieved` =
+    ncu warp instructions per crossing (profiles/ncu_issue.json) x crossings
+    per launch / launch time (CUDA events, live), `peak` = SMs x 4 issue
+    slots x the SM clock sampled during the timed region.  The bandwidth
+    views (compulsory and gathered bytes against HBM, gathered bytes against
+    the measured L2 gather rate) are kept beside it as context."""
+    peak_hbm, peak_src = measured_peaks()
+    per_launch_s = per_launch_ms / 1e3
+    comp = COMPULSORY_BACK if dom == "backward" else COMPULSORY_FWD
+    gath = BYTES_BACK if dom == "backward" else BYTES_FWD
+    comp_gbs = comp * cross_launch / per_launch_s / 1e9
+    gath_gbs = gath * cross_launch / per_launch_s / 1e9
+    l2pk = l2_gather_peak()
+    hbm = {"bytes_per_crossing": comp, "achieved": comp_gbs, "peak": peak_hbm, "unit": "GB/s",
+           "frac": comp_gbs / peak_hbm, "peak_source": peak_src,
+           "gathered_bytes_per_crossing": gath, "gathered_achieved": gath_gbs,
+           "gathered_frac": gath_gbs / peak_hbm}
+    l2 = {"gathered_achieved": gath_gbs, "peak": l2pk, "unit": "GB/s",
+          "frac": gath_gbs / l2pk if l2pk else None,
+          "peak_source": "profiles/microbench.json gather32_L2_GBps"}
+    line = {"kernel": f"trace_kernel<{dom}>", "per_launch_ms": per_launch_ms,
+            "crossings_per_launch": cross_launch,
+            "traffic": ncu_traffic(config, dom, cross_launch),
+            "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per crossing "
+                            "(profiles/ncu_traffic.json) x crossings per launch",
+            "hbm": hbm, "l2": l2}
+    iss = ncu_issue(config, dom)
+    if iss:
+        sms = sm_count()
+        f = (clk_mhz or 1965.0) * 1e6
+        ach = iss["warp_inst_per_crossing"] * cross_launch / per_launch_s
+        peak = sms * ISSUE_SLOTS_PER_SM * f
+        line.update({"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-inst/s",
+                     "frac": ach / peak,
+                     "peak_source": f"{sms} SMs x {ISSUE_SLOTS_PER_SM} issue slots x "
+                                    f"{f / 1e6:.0f} MHz (SM clock sampled in the timed region)",
+                     "issue": iss})
+        l2["lts_throughput_pct_ncu"] = iss.get("lts_throughput_pct")
+    else:   # no capture for this config: the HBM view is the only one available
+        line.update({"bound": "hbm", "achieved": comp_gbs, "peak": peak_hbm, "unit": "GB/s",
+                     "frac": comp_gbs / peak_hbm, "peak_source": peak_src})
+    return line
 
 
 def cpu_baseline(w, geom, y, budget_s=15.0):
     """The oracle as it stands, on this host's cores, on a bounded sample of
     the same scan: an evenly strided subset of ray ids (all angles), sized
-    from a short calibration run to ~budget_s seconds of fwd+back work."""
+    from a short calibration run to ~budget_s seconds of fwd+back work.
+    Built -O3 -march=native on this host; the oracle finds each
+    ray's entering hull face by scanning every hull face, so meshes with many
+    hull faces (c2: 5,944) cost it more per crossing."""
     from oracle import tetref as O
+    O.use_native()
     om = O.OracleMesh.from_mesh(w.mesh)
     cores = len(os.sched_getaffinity(0))
     mu = w.mu.astype(np.float64)
@@ -193,23 +319,31 @@ def cpu_baseline(w, geom, y, budget_s=15.0):
     dt, cross, n = run(n2)
     return {"value": cross / dt, "unit": "tet-crossings/s", "cores": cores, "kind": "oracle",
             "sample": f"{n} of {geom.n_rays} rays (evenly strided over all angles), "
-                      f"fwd+back, {dt:.1f} s", "crossings": int(cross), "seconds": dt}
+                      f"fwd+back, {dt:.1f} s; oracle {O.build_flags()} (brute-force hull "
+                      f"scan over {w.mesh.n_bfaces} faces per ray)",
+            "crossings": int(cross), "seconds": dt}
 
 
 def run_reference(args):
-    """--impl reference: the oracle (CPU, host cores) timed on the same config."""
+    """--impl reference: the oracle (CPU, host cores) timed on the same
+    config.  Under torchrun only rank 0 runs."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    w, _, geom, y = rank_workload(args.config, 0, 1, args.angles)
+    n_gpus = max(args.gpus, ws)
+    w, full, _, _ = rank_workload(args.config, 0, n_gpus, args.angles, args.scaling)
+    y = np.random.default_rng(1000).uniform(0.5, 1.5, (full.n_angles, full.n_v, full.n_u)) \
+        .astype(np.float32)
     from oracle import tetref as O
+    O.use_native()
     om = O.OracleMesh.from_mesh(w.mesh)
     cores = len(os.sched_getaffinity(0))
     n_ang = 2
     times, cross = [], []
     for step in range(args.warmup + args.steps):
-        idx = np.array([(step * 37) % geom.n_angles, (step * 37 + 180) % geom.n_angles])
-        sub = geom.subset(idx)
+        idx = np.array([(step * 37) % full.n_angles,
+                        (step * 37 + full.n_angles // 2) % full.n_angles])
+        sub = full.subset(idx)
         t0 = time.perf_counter()
         _, st = O.project(om, sub, w.mu.astype(np.float64), nthreads=cores)
         _, st2 = O.backproject(om, sub, y[idx], nthreads=cores)
@@ -218,25 +352,44 @@ def run_reference(args):
             times.append(dt)
             cross.append(st["crossings"] + st2["crossings"])
     value = sum(cross) / sum(times)
+    cfg = config_dict(args, w, full, full.subset(np.arange(0, full.n_angles, n_gpus)), n_gpus)
+    cfg["reference_step"] = (f"{n_ang} of {full.n_angles} angles per step (fwd+back), "
+                             f"oracle on {cores} host cores")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tet-crossings/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {w.desc}", "tets": w.mesh.n_tets,
-                       "reference_step": f"{n_ang} of {geom.n_angles} angles per step"},
+            "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * statistics.median(times), "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": cfg,
             "cpu_baseline": {"value": value, "unit": "tet-crossings/s", "cores": cores,
                              "kind": "oracle",
-                             "sample": f"{n_ang} angles x {geom.n_v}x{geom.n_u} pixels per step"},
+                             "sample": f"{n_ang} angles x {full.n_v}x{full.n_u} pixels per step; "
+                                       f"oracle {O.build_flags()}"},
             "e2e": {"value": value, "unit": "tet-crossings/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
+def nccl_report(rank, log_path):
+    """NCCL version and, from the INIT log of this rank, whether NVLS
+    (NVSwitch in-switch reduction) was set up."""
+    import torch
+    out = {"version": ".".join(str(v) for v in torch.cuda.nccl.version())}
+    try:
+        txt = open(log_path).read()
+        out["log"] = os.path.relpath(log_path, ROOT)
+        out["nvls"] = "NVLS" in txt and "NVLS multicast support is not available" not in txt
+        out["init_lines"] = sum(1 for ln in txt.splitlines() if "Init COMPLETE" in ln)
+    except Exception:
+        out["log"] = None
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    maybe_relaunch(args)
     import torch
     import torch.distributed as dist
 
@@ -244,20 +397,32 @@ def main():
     from paper_1908_06909_b200.dist import dist_backproject
 
     ws, rank, local = dist_env()
+    if ws != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}\n")
+        return 2
     # one process per GPU over NCCL; TETPROJ_DIST_BACKEND=gloo (testing the
     # multi-rank logic with several ranks on one GPU) maps ranks onto devices
     backend = os.environ.get("TETPROJ_DIST_BACKEND", "nccl")
+    if backend == "nccl" and ws > torch.cuda.device_count():
+        sys.stderr.write(f"bench.py: {ws} NCCL ranks but {torch.cuda.device_count()} GPUs\n")
+        return 2
     local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    nccl_log = None
     if ws > 1:
         if backend == "nccl":
+            if "NCCL_DEBUG" not in os.environ:   # communicator init log (NVLS or not)
+                nccl_log = os.path.join(ROOT, "gpurun_out", f"nccl_init_rank{rank}.log")
+                os.makedirs(os.path.dirname(nccl_log), exist_ok=True)
+                os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,NVLS",
+                                  NCCL_DEBUG_FILE=nccl_log)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     if ws > 1 and rank != 0:
         dist.barrier()                      # rank 0 builds the mesh cache first
-    w, full_geom, geom, y_np = rank_workload(args.config, rank, ws, args.angles)
+    w, full_geom, geom, y_np = rank_workload(args.config, rank, ws, args.angles, args.scaling)
     if ws > 1 and rank == 0:
         dist.barrier()
     torch.cuda.synchronize()
@@ -301,6 +466,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
+        t_wall = time.perf_counter()
         for i in range(args.steps):
             flush.zero_()                    # L2 flush between timed steps (not timed)
             ev[i][0].record(stream)
@@ -309,29 +475,31 @@ def main():
             backward()
             ev[i][2].record(stream)
         torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
         clocks.stop()
         if ws > 1:
             dist.barrier()
     T.tet_set_kernel_timing(h, False)
     kt = T.tet_kernel_times(h)
-    ms_f = [a.elapsed_time(b) for a, b, c in ev]
-    ms_b = [b.elapsed_time(c) for a, b, c in ev]
-    ms_step = [f + b for f, b in zip(ms_f, ms_b)]
-    t_local = sum(ms_step) / 1e3
-    crossings_local = (st_f["crossings"] + st_b["crossings"]) * args.steps
-    vals = torch.tensor([t_local, sum(ms_f) / 1e3, sum(ms_b) / 1e3, crossings_local,
-                         st_f["crossings"], st_b["crossings"], geom.n_rays, st_f["rays_hit"],
-                         st_f["lost"] + st_b["lost"], st_f["stuck"] + st_b["stuck"],
-                         st_f["exact_fallbacks"] + st_b["exact_fallbacks"]],
-                        dtype=torch.float64, device=dev)
+    # per-step device times, max over ranks step by step, then the median step
+    per = torch.tensor([[a.elapsed_time(b) for a, b, c in ev],
+                        [b.elapsed_time(c) for a, b, c in ev]], dtype=torch.float64, device=dev)
+    counts = torch.tensor([st_f["crossings"], st_b["crossings"], geom.n_rays, st_f["rays_hit"],
+                           st_f["lost"] + st_b["lost"], st_f["stuck"] + st_b["stuck"],
+                           st_f["exact_fallbacks"] + st_b["exact_fallbacks"]],
+                          dtype=torch.float64, device=dev)
     if ws > 1:
-        mx = vals[:3].clone()
-        sm = vals[3:].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        vals = torch.cat([mx, sm])
-    (t_max, tf_max, tb_max, cross_all, cf_all, cb_all, rays_all, hit_all, lost_all, stuck_all,
-     exact_all) = vals.tolist()
+        steps_max = (per[0] + per[1]).clone()
+        dist.all_reduce(per, op=dist.ReduceOp.MAX)
+        dist.all_reduce(steps_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+    else:
+        steps_max = per[0] + per[1]
+    ms_f = per[0].tolist()
+    ms_b = per[1].tolist()
+    ms_step = steps_max.tolist()
+    cf_all, cb_all, rays_all, hit_all, lost_all, stuck_all, exact_all = counts.tolist()
+    med = statistics.median(ms_step)
 
     # ---- e2e: same metric through the public API with HOST buffers ----
     mu_h = torch.from_numpy(w.mu).pin_memory()
@@ -354,88 +522,66 @@ def main():
         torch.cuda.synchronize()
         if i > 0:
             e2e_ms.append(a.elapsed_time(b))
-    e2e_t = torch.tensor([max(sum(e2e_ms), 1e-9) / 1e3], dtype=torch.float64, device=dev)
+    e2e_t = torch.tensor(e2e_ms or [0.0], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = (cf_all + cb_all) * len(e2e_ms) / e2e_t.item() if e2e_ms else None
+    e2e_value = (cf_all + cb_all) / (statistics.median(e2e_t.tolist()) / 1e3) if e2e_ms else None
 
     if rank == 0:
-        peak, peak_src = measured_peaks()
         tf, nf = kt["forward"]
         tb, nb = kt["backward"]
         te, ne = kt["entry"]
         tp, np_ = kt["permute"]
-        per_launch_f = tf / max(nf, 1)
-        per_launch_b = tb / max(nb, 1)
         # dominant kernel: the walk with the larger share of the step
         if tb >= tf:
-            dom, bytes_unit, cross_unit, launches, tdom = "backward", BYTES_BACK, st_b["crossings"], nb, tb
+            dom, cross_unit, launches, tdom = "backward", st_b["crossings"], nb, tb
         else:
-            dom, bytes_unit, cross_unit, launches, tdom = "forward", BYTES_FWD, st_f["crossings"], nf, tf
-        comp_unit = COMPULSORY_BACK if dom == "backward" else COMPULSORY_FWD
-        l2pk = l2_gather_peak()
-        algo_bytes_per_launch = bytes_unit * cross_unit / max(launches // args.steps, 1)
-        achieved = algo_bytes_per_launch / (tdom / max(launches, 1) / 1e3) / 1e9
-        achieved_c = achieved * comp_unit / bytes_unit
+            dom, cross_unit, launches, tdom = "forward", st_f["crossings"], nf, tf
+        per_step_launches = max(launches // args.steps, 1)
+        clk = clocks.summary()
+        rl = roofline(args.config, dom, cross_unit / per_step_launches,
+                      tdom / max(launches, 1), clk.get("sm_mhz"))
         # each timed entry region launches two kernels (setup + raster)
         n_launch_step = (nf + nb + 2 * ne + np_) / args.steps
-        clk = clocks.summary()
         line = {
             "metric": METRIC,
-            "value": cross_all / t_max,
+            "value": (cf_all + cb_all) / (med / 1e3),
             "unit": "tet-crossings/s",
             "n_gpus": ws,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": 1e3 * t_max / args.steps,
+            "ms_per_step": med,
+            "ms_per_step_mean": statistics.mean(ms_step),
+            "ms_per_step_all": ms_step,
+            "timed_region_wall_s": t_wall,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": args.scaling,
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"{args.config}: {w.desc}", "tets": w.mesh.n_tets,
-                       "verts": w.mesh.n_verts, "hull_faces": w.mesh.n_bfaces,
-                       "angles_per_gpu": geom.n_angles, "detector": [geom.n_v, geom.n_u],
-                       "rays_per_step": int(rays_all), "parallelism": f"angles x{ws}",
-                       "l2": "flushed between timed steps (256 MiB write, untimed)"},
-            "fwd": {"crossings_per_s": cf_all * args.steps / tf_max,
-                    "mrays_per_s": rays_all * args.steps / tf_max / 1e6,
-                    "ms": 1e3 * tf_max / args.steps, "crossings": int(cf_all)},
-            "back": {"crossings_per_s": cb_all * args.steps / tb_max,
-                     "mrays_per_s": rays_all * args.steps / tb_max / 1e6,
-                     "ms": 1e3 * tb_max / args.steps, "crossings": int(cb_all)},
+            "config": config_dict(args, w, full_geom, geom, ws),
+            "fwd": {"crossings_per_s": cf_all / (statistics.median(ms_f) / 1e3),
+                    "mrays_per_s": rays_all / (statistics.median(ms_f) / 1e3) / 1e6,
+                    "ms": statistics.median(ms_f), "crossings": int(cf_all)},
+            "back": {"crossings_per_s": cb_all / (statistics.median(ms_b) / 1e3),
+                     "mrays_per_s": rays_all / (statistics.median(ms_b) / 1e3) / 1e6,
+                     "ms": statistics.median(ms_b), "crossings": int(cb_all)},
             "rays_hit": int(hit_all), "lost": int(lost_all), "stuck": int(stuck_all),
             "exact_fallbacks_per_step": int(exact_all),
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
             "mesh_create_s": t_create,
-            "roofline": {"bound": "hbm", "kernel": f"trace_kernel<{dom}>",
-                         "achieved": achieved_c, "peak": peak, "unit": "GB/s",
-                         "frac": achieved_c / peak, "peak_source": peak_src,
-                         "bytes_per_crossing": comp_unit,
-                         "traffic": ncu_traffic(args.config, dom,
-                                                cross_unit / max(launches // args.steps, 1)),
-                         "per_launch_ms": per_launch_b if dom == "backward" else per_launch_f,
-                         "note": "compulsory bytes per crossing (SURVEY 8(d)) x crossings per "
-                                 "step / busy time of the walk-kernel class per step (union of its "
-                                 "launch intervals, CUDA events on the launching streams: angle "
-                                 "chunks alternate between two streams and may overlap); "
-                                 "per_launch_ms = busy time / launches.  ncu DRAM traffic per "
-                                 "crossing: c3 0.27 fwd / 0.22 back (L2-resident); c5 0.30 fwd "
-                                 "(band order keeps a mesh slab in L2 across angles) / 2.9 back "
-                                 "(0.39 TB/s, 6 % of HBM) within 3 % of c3's crossing rate: the walk "
-                                 "is latency/issue-bound, not bandwidth-bound (DESIGN.md 5, "
-                                 "Roofline); traffic = that per-crossing figure x crossings/launch",
-                         "gathered_bytes_per_crossing": bytes_unit,
-                         "gathered_achieved": achieved,
-                         "gathered_frac": achieved / peak,
-                         "l2_gather_peak_gbs": l2pk,
-                         "l2_gather_frac": achieved / l2pk if l2pk else None},
+            "roofline": rl,
             "e2e": {"value": e2e_value, "unit": "tet-crossings/s",
                     "h2d_bytes_per_step": int(w.mu.nbytes + y_np.nbytes),
                     "d2h_bytes_per_step": int(proj.numel() * 4 + x.numel() * 4)},
             "gpu_launches": int(round(n_launch_step * args.steps)),
             "clocks": clk,
         }
+        if ws > 1:
+            line["collective"] = {"backend": backend, "op": "all_reduce(SUM) f32 [n_tets]",
+                                  "bytes": int(x.numel() * 4)}
+            if backend == "nccl":
+                line["collective"]["nccl"] = nccl_report(rank, nccl_log)
         if not args.no_cpu_baseline and ws == 1:
             line["cpu_baseline"] = cpu_baseline(w, geom, y_np)
         print(json.dumps(line), flush=True)

@@ -2,7 +2,9 @@
 """Measured roofline denominators for the walker:
 
   gather32_L2   random 32-B gathers (one 256-bit load each) from a 64 MB buffer
+                (2^21 records; 32-bit xorshift index masked to the power of two)
   gather32_HBM  the same from a 8 GB buffer (DRAM-resident)
+  gather16_L2   random 16-B gathers from a 64 MB buffer (the vertex gather)
   stream_L2     coalesced reads of a 64 MB buffer, 50 passes (L2 bandwidth)
   dfma          fp64 FMA rate (8 independent chains per thread)
   red_f64       RED.ADD.F64 to random addresses of an 8 MB array (L2 atomics)
@@ -43,6 +45,9 @@ def main():
     ms = L.tetmicro_run(0, 8 << 30, iters, blocks, threads)
     out["gather32_HBM_GBps"] = n * 32 / (ms / 1e3) / 1e9
     out["gather32_HBM_Grec_per_s"] = n / (ms / 1e3) / 1e9
+    ms = L.tetmicro_run(7, 64 << 20, iters, blocks, threads)
+    out["gather16_L2_GBps"] = n * 16 / (ms / 1e3) / 1e9
+    out["gather16_L2_Grec_per_s"] = n / (ms / 1e3) / 1e9
     passes = 50
     ms = L.tetmicro_run(1, 64 << 20, passes, sms * 8, 512)
     out["stream_L2_GBps"] = (64 << 20) * passes / (ms / 1e3) / 1e9

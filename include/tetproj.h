@@ -129,8 +129,10 @@ typedef struct {
  *   bfaces [n_bfaces][2] int32   (t, k) with nbrs[t][k] == -1 (host)
  * Host arrays are read during the call and not retained.  Validation (exact
  * orientation, reciprocity, hull == {nbr == -1}, closed manifold hull, exact
- * convexity) happens here, before any device allocation.  On success *out
- * owns all device memory of the mesh until tet_mesh_destroy.               */
+ * convexity) happens here, before the device is touched: a mesh error is
+ * reported (TET_E_MESH / TET_E_NONCONVEX) even when `device` does not exist;
+ * a valid mesh on a missing device gives TET_E_CUDA.  On success *out owns
+ * all device memory of the mesh until tet_mesh_destroy.                    */
 tet_status tet_mesh_create(const double* verts, int64_t n_verts,
                            const int32_t* tets, const int32_t* nbrs, int64_t n_tets,
                            const int32_t* bfaces, int64_t n_bfaces,
@@ -157,8 +159,11 @@ tet_status tet_backproject(tet_mesh_t m, const tet_geometry* g, const float* pro
                            int accumulate, void* cuda_stream, tet_stats* st);
 
 /* Backprojection into a caller-provided double accumulator (device pointer,
- * caller order) without rounding: acc += A^T proj.  Used by the multi-GPU
- * driver to all-reduce double partial sums.                                  */
+ * caller order) without rounding: acc += A^T proj.  For callers that reduce
+ * partial sums in double (paper_1908_06909_b200.dist.dist_backproject with
+ * precision="f64"); the default multi-GPU path all-reduces the f32 result of
+ * tet_backproject (each rank's sum rounded once: <= W * 2^-24 relative for W
+ * ranks, R15).                                                     */
 tet_status tet_backproject_f64(tet_mesh_t m, const tet_geometry* g, const float* proj,
                                double* acc, void* cuda_stream, tet_stats* st);
 

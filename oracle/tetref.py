@@ -8,7 +8,9 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import socket
 import subprocess
+import tempfile
 
 import numpy as np
 
@@ -19,14 +21,43 @@ CFLAGS = ["-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-std=gnu11"
           "-shared", "-fPIC", "-Wall", "-Wno-unused-function"]
 
 
+# host-specific build: outside the tree, so it never travels to another machine
+NATIVE_LIB = os.path.join(tempfile.gettempdir(),
+                          f"tetproj_oracle_native_{socket.gethostname()}.so")
+_native = False
+
+
+def _stale(lib):
+    return not os.path.exists(lib) or os.path.getmtime(lib) < max(
+        os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "tetref.h")))
+
+
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (no -march=native: the .so travels)."""
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(
-            os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "tetref.h"))):
+    if force or _stale(LIB):
         tmp = LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", *CFLAGS, SRC, "-o", tmp, "-lm"])
         os.replace(tmp, LIB)
     return LIB
+
+
+def use_native() -> None:
+    """Load the same source compiled -O3 -march=native for THIS host (the
+    CPU-baseline timing build of SURVEY 8(d)); built on the machine that runs
+    it, never shipped.  Must be called before the first oracle call."""
+    global _native
+    if _lib is not None:
+        return
+    if _stale(NATIVE_LIB):
+        tmp = NATIVE_LIB + f".tmp{os.getpid()}"
+        flags = ["-O3", "-march=native"] + [f for f in CFLAGS if f != "-O2"]
+        subprocess.check_call(["gcc", *flags, SRC, "-o", tmp, "-lm"])
+        os.replace(tmp, NATIVE_LIB)
+    _native = True
+
+
+def build_flags() -> str:
+    return "gcc -O3 -march=native -fopenmp" if _native else "gcc -O2 -fopenmp"
 
 
 class _Geom(C.Structure):
@@ -48,7 +79,7 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        _lib = C.CDLL(build())
+        _lib = C.CDLL(NATIVE_LIB if _native else build())
         P = C.c_void_p
         _lib.tetref_mesh_create.argtypes = [P, C.c_int64, P, P, C.c_int64, P, C.c_int64,
                                             C.c_uint32, C.POINTER(C.c_void_p)]

@@ -29,6 +29,11 @@ struct tet_mesh {
     void* d_perm = nullptr;
     void* d_bvh_nodes = nullptr;
     void* d_bvh_faces = nullptr;
+    // private stream-ordered pool for per-call scratch: freed scratch stays
+    // cached across this mesh's calls (no re-allocation inside timed calls)
+    // and is returned to the device at tet_mesh_destroy; the device's default
+    // pool -- shared with the rest of the process -- is never touched
+    cudaMemPool_t pool = nullptr;
     int64_t bytes = 0;
     // kernel timing (tet_set_kernel_timing)
     struct TimerRec { int kind; cudaEvent_t a, b; };
@@ -110,13 +115,14 @@ bool is_device_ptr(const void* p, int dev, bool& wrong_device) {
     return false;
 }
 
-// Scratch allocated stream-ordered from the device's default pool.
+// Scratch allocated stream-ordered from the mesh's private pool.
 struct Scratch {
     cudaStream_t s;
+    cudaMemPool_t pool;
     std::vector<void*> ptrs;
-    explicit Scratch(cudaStream_t st) : s(st) {}
+    Scratch(cudaStream_t st, cudaMemPool_t p) : s(st), pool(p) {}
     cudaError_t alloc(void** p, size_t n) {
-        cudaError_t e = cudaMallocAsync(p, n ? n : 16, s);
+        cudaError_t e = cudaMallocFromPoolAsync(p, n ? n : 16, pool, s);
         if (e == cudaSuccess) ptrs.push_back(*p);
         return e;
     }
@@ -125,15 +131,15 @@ struct Scratch {
     }
 };
 
-void pool_setup(int dev) {
-    static bool done[64] = {false};
-    if (dev < 0 || dev >= 64 || done[dev]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;  // keep freed scratch cached across calls
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done[dev] = true;
+cudaError_t make_pool(int dev, cudaMemPool_t* pool) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaError_t e = cudaMemPoolCreate(pool, &props);
+    if (e != cudaSuccess) return e;
+    uint64_t thr = UINT64_MAX;   // keep this mesh's freed scratch until destroy
+    return cudaMemPoolSetAttribute(*pool, cudaMemPoolAttrReleaseThreshold, &thr);
 }
 
 enum class Op { Forward, Backward, BackwardF64 };
@@ -277,7 +283,6 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
     tet_status rs = prepare_geometry(m->host, g, ang, aux, err);
     if (rs != TET_OK) return fail(rs, err);
     DeviceGuard guard(m->device);
-    pool_setup(m->device);
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t nrays = (int64_t)g->n_angles * g->n_v * g->n_u;
     const int64_t nt = m->dev.nt;
@@ -292,7 +297,7 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
     const bool need_stats = st || strict;
     unsigned long long hs[ST_COUNT] = {0};
     {
-        Scratch sc(s);  // released (stream-ordered) at the end of this scope
+        Scratch sc(s, m->pool);  // released (stream-ordered) at the end of this scope
         // --- stage host inputs / outputs through device memory.  The
         // per-ray host arrays (y of a backprojection, proj of a projection)
         // move chunk by chunk on a copy stream, overlapped with the tracing
@@ -458,11 +463,8 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
                            int64_t n_bfaces, int device, uint32_t flags, tet_mesh_t* out) {
     if (!out) return fail(TET_E_ARG, "null output handle");
     *out = nullptr;
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
-        cudaGetLastError();
-        return fail(TET_E_CUDA, "no such CUDA device: " + std::to_string(device));
-    }
+    // host-side validation first: mesh errors are reported as such even on a
+    // machine without a usable device
     tet_mesh* m = new tet_mesh();
     std::string err;
     tet_status s = prepare_mesh(verts, n_verts, tets, nbrs, n_tets, bfaces, n_bfaces, flags,
@@ -470,6 +472,12 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     if (s != TET_OK) {
         delete m;
         return fail(s, err);
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        delete m;
+        return fail(TET_E_CUDA, "no such CUDA device: " + std::to_string(device));
     }
     m->device = device;
     m->flags = flags;
@@ -481,7 +489,8 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
         m->bytes += (int64_t)n;
         return e;
     };
-    cudaError_t e = up(&m->d_rec, H.rec.data(), H.rec.size() * 4);
+    cudaError_t e = make_pool(device, &m->pool);
+    if (e == cudaSuccess) e = up(&m->d_rec, H.rec.data(), H.rec.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_tnode, H.tnode.data(), H.tnode.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_vtx, H.vtx.data(), H.vtx.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_hull, H.hull.data(), H.hull.size() * 4);
@@ -548,6 +557,8 @@ tet_status tet_mesh_destroy(tet_mesh_t m) {
     cudaFree(m->d_perm);
     cudaFree(m->d_bvh_nodes);
     cudaFree(m->d_bvh_faces);
+    // returned to the device once the last stream-ordered free has run
+    if (m->pool) cudaMemPoolDestroy(m->pool);
     delete m;
     return TET_OK;
 }

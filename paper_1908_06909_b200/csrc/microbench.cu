@@ -13,21 +13,41 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
     return x;
 }
 
-// Each thread issues `iters` dependent-free 32-B gathers (one 256-bit load at
-// a hashed record index) and folds them into a checksum.
-__global__ void gather32_kernel(const int4* __restrict__ buf, uint64_t n_rec, int iters,
+// Each thread issues `iters` independent 32-B gathers (one 256-bit load at a
+// pseudo-random record index) and folds them into a checksum.  The record
+// count is a power of two: the index is a 32-bit xorshift state masked to
+// the buffer (7 integer ops per load, no 64-bit modulo), so the loop is
+// bound by the memory system, not by index arithmetic.
+__global__ void gather32_kernel(const int4* __restrict__ buf, uint32_t mask, int iters,
                                 unsigned* __restrict__ sink) {
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t s = hash32(tid) | 1u;
     unsigned acc = 0;
-#pragma unroll 4
+#pragma unroll 8
     for (int i = 0; i < iters; ++i) {
-        const uint64_t r = hash32(tid * 0x9E3779B1u + i) % n_rec;
+        s ^= s << 13; s ^= s >> 17; s ^= s << 5;
+        const uint32_t r = s & mask;
         int a0, a1, a2, a3, a4, a5, a6, a7;
         asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3), "=r"(a4), "=r"(a5), "=r"(a6),
                        "=r"(a7)
-                     : "l"(buf + 2 * r));
+                     : "l"(buf + 2 * (size_t)r));
         acc += a0 ^ a1 ^ a2 ^ a3 ^ a4 ^ a5 ^ a6 ^ a7;
+    }
+    if (acc == 0x12345678u) sink[0] = acc;
+}
+
+// The same with 16-B records (the walker's vertex gather).
+__global__ void gather16_kernel(const int4* __restrict__ buf, uint32_t mask, int iters,
+                                unsigned* __restrict__ sink) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t s = hash32(tid) | 1u;
+    unsigned acc = 0;
+#pragma unroll 8
+    for (int i = 0; i < iters; ++i) {
+        s ^= s << 13; s ^= s >> 17; s ^= s << 5;
+        const int4 v = __ldg(buf + (s & mask));
+        acc += v.x ^ v.y ^ v.z ^ v.w;
     }
     if (acc == 0x12345678u) sink[0] = acc;
 }
@@ -91,8 +111,9 @@ __global__ void red32_kernel(float* __restrict__ acc, uint64_t n, int iters) {
 extern "C" {
 
 // Returns the kernel time in ms (CUDA events), or a negative value on error.
-// kind: 0 gather32 (bytes = n_rec_used*32 buffer), 1 stream, 2 dfma, 3 red.f64,
-// 4 red.f32, 5 red.f64 coherent (8 addresses x 4 lanes per warp), 6 red.f32 coherent
+// kind: 0 gather32 (power-of-two buffer of 32-B records), 1 stream, 2 dfma,
+// 3 red.f64, 4 red.f32, 5 red.f64 coherent (8 addresses x 4 lanes per warp),
+// 6 red.f32 coherent, 7 gather16 (power-of-two buffer of 16-B records)
 double tetmicro_run(int kind, uint64_t buffer_bytes, int iters, int blocks, int threads) {
     void* buf = nullptr;
     unsigned* sink = nullptr;
@@ -104,8 +125,12 @@ double tetmicro_run(int kind, uint64_t buffer_bytes, int iters, int blocks, int 
     cudaEventCreate(&b);
     for (int rep = 0; rep < 2; ++rep) {   // rep 0 = warm-up
         cudaEventRecord(a);
-        if (kind == 0)
-            gather32_kernel<<<blocks, threads>>>((const int4*)buf, buffer_bytes / 32, iters, sink);
+        if (kind == 0)   // buffer_bytes must be a power of two
+            gather32_kernel<<<blocks, threads>>>((const int4*)buf, (uint32_t)(buffer_bytes / 32 - 1),
+                                                 iters, sink);
+        else if (kind == 7)
+            gather16_kernel<<<blocks, threads>>>((const int4*)buf, (uint32_t)(buffer_bytes / 16 - 1),
+                                                 iters, sink);
         else if (kind == 1)
             stream_kernel<<<blocks, threads>>>((const int4*)buf, buffer_bytes / 16, iters, sink);
         else if (kind == 2)
@@ -116,7 +141,7 @@ double tetmicro_run(int kind, uint64_t buffer_bytes, int iters, int blocks, int 
             red32_kernel<<<blocks, threads>>>((float*)buf, buffer_bytes / 4, iters);
         else if (kind == 5)
             red_coherent_kernel<double><<<blocks, threads>>>((double*)buf, buffer_bytes / 8, iters);
-        else
+        else if (kind == 6)
             red_coherent_kernel<float><<<blocks, threads>>>((float*)buf, buffer_bytes / 4, iters);
         cudaEventRecord(b);
     }

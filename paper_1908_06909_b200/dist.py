@@ -32,6 +32,11 @@ class AngleSharding:
     def __post_init__(self):
         if not (0 <= self.rank < self.world) or self.n_angles < 1:
             raise ValueError("bad sharding")
+        if self.n_angles < self.world:
+            # a rank without angles would have no local operator call to make
+            # (the library rejects empty scans) and its peers would wait in
+            # the all-reduce forever
+            raise ValueError(f"{self.n_angles} angles cannot be sharded over {self.world} ranks")
 
     def local_angles(self) -> np.ndarray:
         return np.arange(self.rank, self.n_angles, self.world)
@@ -66,14 +71,28 @@ def dist_project(mesh, geom, mu, group=None, project=None):
     return fn(sh.local_geometry(geom), mu), sh
 
 
-def dist_backproject(mesh, geom, y_local, group=None, backproject=None, async_op=False):
+def dist_backproject(mesh, geom, y_local, group=None, backproject=None, async_op=False,
+                     precision: str = "f32"):
     """x = A^T y over all ranks: local backprojection of this rank's angles,
     then all_reduce(SUM).  ``y_local`` holds this rank's rows
     (``AngleSharding.local_stack``).  Returns the reduced per-tet tensor
-    (or (tensor, work) when ``async_op``)."""
+    (or (tensor, work) when ``async_op``).
+
+    precision "f32" (default): each rank's tet_backproject result (double
+    accumulation on the device, rounded once to float) is summed in float --
+    W ranks add at most W * 2^-24 relative (R15).  "f64": each rank
+    accumulates into a double tensor (tet_backproject_f64) and the double
+    partial sums are reduced; the result stays float64."""
     import torch.distributed as dist
     sh = sharding_for(geom, group)
-    fn = backproject if backproject is not None else mesh.backproject
-    x = fn(sh.local_geometry(geom), y_local)
+    lg = sh.local_geometry(geom)
+    if backproject is not None:
+        x = backproject(lg, y_local)
+    elif precision == "f64":
+        x = mesh.backproject_f64(lg, y_local)
+    elif precision == "f32":
+        x = mesh.backproject(lg, y_local)
+    else:
+        raise ValueError(f"precision must be 'f32' or 'f64', not {precision!r}")
     work = dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
     return (x, work) if async_op else x

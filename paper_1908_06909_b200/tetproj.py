@@ -290,6 +290,16 @@ class TetMesh:
         st = tet_project(self.handle, geom, mu, out, stats=stats, opts=opts)
         return (out, st) if stats else out
 
+    def backproject_f64(self, geom, proj, out=None, stats: bool = False):
+        """acc = A^T proj in double (tet_backproject_f64 into a zeroed float64
+        device tensor, or += into ``out``)."""
+        import torch
+        if out is None:
+            out = torch.zeros(self.n_tets, dtype=torch.float64,
+                              device=proj.device if isinstance(proj, torch.Tensor) else "cpu")
+        st = tet_backproject_f64(self.handle, geom, proj, out, stats=stats)
+        return (out, st) if stats else out
+
     def backproject(self, geom, proj, out=None, accumulate=False, stats: bool = False, opts=None):
         import torch
         if out is None:

@@ -29,7 +29,7 @@ def back_errors(g, r):
     return err
 
 
-def run_gpu(mesh, geom, mu, y, device="cuda:0", flags=None):
+def run_gpu(mesh, geom, mu, y, device="cuda:0", flags=None, opts=None):
     import torch
 
     from paper_1908_06909_b200 import TetMesh
@@ -37,9 +37,9 @@ def run_gpu(mesh, geom, mu, y, device="cuda:0", flags=None):
     tm = TetMesh.from_mesh(mesh, device=0, **kw)
     dev = torch.device(device)
     proj, st = tm.project(geom, torch.from_numpy(np.ascontiguousarray(mu, np.float32)).to(dev),
-                          stats=True)
+                          stats=True, opts=opts)
     x, st2 = tm.backproject(geom, torch.from_numpy(np.ascontiguousarray(y, np.float32)).to(dev),
-                            stats=True)
+                            stats=True, opts=opts)
     torch.cuda.synchronize()
     return proj.cpu().numpy(), x.cpu().numpy(), st, st2, tm
 
@@ -51,8 +51,11 @@ def run_oracle(mesh, geom, mu, y):
     return p, x, st, st2
 
 
-def check_parity(mesh, geom, mu, y, *, expect_exact_fallbacks=None):
-    p, x, st, st2, _ = run_gpu(mesh, geom, mu, y)
+def check_parity(mesh, geom, mu, y, *, expect_exact_fallbacks=None, opts=None):
+    """CUDA path (``opts``: traversal / entry-finder options, default exact +
+    raster) vs the oracle: identical crossing and hit counts, per-pixel and
+    per-tet values within the north-star tolerances, adjoint."""
+    p, x, st, st2, _ = run_gpu(mesh, geom, mu, y, opts=opts)
     pr, xr, ost, ost2 = run_oracle(mesh, geom, mu, y)
     for s in (st, st2):
         assert s["lost"] == 0 and s["stuck"] == 0 and s["entry_conflicts"] == 0, s

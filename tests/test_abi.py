@@ -57,6 +57,32 @@ def test_no_cpu_fallback_without_gpu():
     assert e.value.status == tetproj.TET_E_CUDA
 
 
+@pytest.mark.parametrize("case,want", [("l_shaped", "TET_E_NONCONVEX"),
+                                       ("two_tets", "TET_E_NONCONVEX"),
+                                       ("carved", "TET_E_MESH")])
+def test_library_mesh_validation_statuses(case, want):
+    """tet_mesh_create validates on the host before touching the device, so
+    its exact checks are pinned here without a GPU: the L-shaped lattice
+    (reflex hull edges) and two disjoint tets (no reflex edge: only the global
+    all-vertices-against-all-hull-planes check catches it) are rejected as
+    non-convex, a carved lattice as a non-manifold mesh."""
+    from paper_1908_06909_b200 import tetproj
+    from workloads import meshes as M
+    if case == "l_shaped":
+        m = M.l_shaped_lattice()
+        t, nb, bf = m.tets, m.nbrs, m.bfaces
+    elif case == "two_tets":
+        m = M.two_disjoint_tets()
+        t, nb, bf = m.tets, m.nbrs, m.bfaces
+    else:
+        m = M.kuhn_lattice(2)
+        t = m.tets[[i for i in range(m.n_tets) if i % 7 != 3]]
+        nb, bf = M.build_graph(t)
+    with pytest.raises(tetproj.TetProjError) as e:
+        tetproj.tet_mesh_create(m.verts, t, nb, bf, device=0)
+    assert e.value.status == getattr(tetproj, want), str(e.value)
+
+
 def test_product_package_does_not_import_oracle():
     pkg = os.path.join(ROOT, "paper_1908_06909_b200")
     for f in glob.glob(os.path.join(pkg, "**", "*"), recursive=True):

@@ -55,9 +55,13 @@ def _worker(rank, world, port, out_path):
 
 
 def test_sharding_partitions_angles():
-    for n, w in [(4, 2), (360, 8), (7, 3), (1, 1), (5, 8)]:
+    for n, w in [(4, 2), (360, 8), (7, 3), (1, 1), (8, 8), (41, 2)]:
         got = np.sort(np.concatenate([AngleSharding(n, r, w).local_angles() for r in range(w)]))
         np.testing.assert_array_equal(got, np.arange(n))
+    # fewer angles than ranks: an empty rank would leave its peers waiting in
+    # the all-reduce, so the sharding refuses it up front
+    with pytest.raises(ValueError):
+        AngleSharding(5, 0, 8)
 
 
 def test_gloo_two_ranks_backprojection_allreduce(tmp_path):

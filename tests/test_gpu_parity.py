@@ -133,6 +133,9 @@ def test_bvh_entry_finder_identical(case):
     b, sb = tm.project(geom, mu_d, stats=True, opts=T.options(entry=T.TET_ENTRY_BVH))
     assert torch.equal(a, b)
     assert sa["crossings"] == sb["crossings"] and sa["rays_hit"] == sb["rays_hit"]
+    # and the BVH-entry path against the oracle (forward, backward, adjoint)
+    y = np.random.default_rng(2).uniform(0.5, 1.5, geom.n_rays).astype(np.float32)
+    U.check_parity(mesh, geom, mu, y, opts=T.options(entry=T.TET_ENTRY_BVH))
 
 
 def test_debug_build_bounds_checks():
@@ -232,7 +235,12 @@ def test_errors_are_statuses():
     nb, bf = M.build_graph(a.tets[keep])
     with pytest.raises(T.TetProjError) as e:
         T.tet_mesh_create(a.verts, a.tets[keep], nb, bf)
-    assert e.value.status in (T.TET_E_NONCONVEX, T.TET_E_MESH)
+    assert e.value.status == T.TET_E_MESH            # non-manifold hull
+    for make in (M.l_shaped_lattice, M.two_disjoint_tets):
+        m = make()
+        with pytest.raises(T.TetProjError) as e:
+            T.tet_mesh_create(m.verts, m.tets, m.nbrs, m.bfaces)
+        assert e.value.status == T.TET_E_NONCONVEX, str(e.value)
     tm = T.TetMesh.from_mesh(M.ball_mesh(h=0.3, seed=3))
     g_inside = G.circular_cone([0.0], 0.5, 8.0, 8, 8, 0.1, 0.1)   # source inside the mesh
     with pytest.raises(T.TetProjError) as e:
@@ -267,7 +275,7 @@ def test_full_size_c3_sampled():
     assert abs(rowsum - colsum) / rowsum <= U.ADJ_TOL
 
 
-def _sampled_backprojection_check(tm, geom, mesh, om, ids):
+def _sampled_backprojection_check(tm, geom, mesh, om, ids, min_nonzero=1000):
     """Backprojection per tet at full size: y = 1 + (ray id mod 7) on the
     sampled rays and 0 elsewhere, so the oracle computes every tet's exact
     value from those rays alone (oracle backproject with ray_ids)."""
@@ -278,7 +286,7 @@ def _sampled_backprojection_check(tm, geom, mesh, om, ids):
     y[ids] = 1.0 + (ids % 7).astype(np.float32)
     x = tm.backproject(geom, torch.from_numpy(y).cuda()).cpu().numpy().astype(np.float64)
     xr, _ = O.backproject(om, geom, y[ids], ray_ids=ids)
-    assert np.count_nonzero(xr) > 1000
+    assert np.count_nonzero(xr) > min_nonzero
     be = U.back_errors(x, xr)
     assert be.max() <= U.BACK_TOL, (be.max(), int(be.argmax()))
 
@@ -292,6 +300,36 @@ def test_full_size_c3_sampled_backprojection():
     om = O.OracleMesh.from_mesh(w.mesh)
     ids = np.sort(np.random.default_rng(11).choice(w.geom.n_rays, 3000, replace=False))
     _sampled_backprojection_check(tm, w.geom, w.mesh, om, ids)
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c4a", "c4b"])
+def test_full_size_sampled(cfg):
+    """The other BASELINE configs at full size (c2 256^2 x 90, c4a 512^2 x 16
+    lattice directions, c4b 512^2 x 32 with sources on lattice points), in
+    bench.py's launch configuration: zero lost / stuck rays and zero entry
+    conflicts over every ray (the c4 bar: "zero lost rays on sliver
+    meshes"), 2000 sampled rays' projections against the oracle one by one,
+    every tet's backprojection of those rays, and the adjoint identity."""
+    from oracle import tetref as O
+    w = CF.workload(cfg)
+    p, x, st, st2, tm = U.run_gpu(w.mesh, w.geom, w.mu, w.y)
+    assert st["lost"] == st["stuck"] == st["entry_conflicts"] == 0, st
+    assert st2["lost"] == st2["stuck"] == 0, st2
+    assert st["crossings"] == st2["crossings"] and st["rays_hit"] > 0
+    om = O.OracleMesh.from_mesh(w.mesh)
+    rng = np.random.default_rng(17)
+    hit = np.flatnonzero(p.ravel() != 0)
+    ids = np.sort(np.concatenate([rng.choice(w.geom.n_rays, 1000, replace=False),
+                                  rng.choice(hit, 1000, replace=False)]))
+    ids = np.unique(ids)
+    pr, ost = O.project(om, w.geom, w.mu.astype(np.float64), ray_ids=ids)
+    assert ost["lost"] == ost["stuck"] == 0
+    fe = U.fwd_errors(p.ravel()[ids].astype(np.float64), pr, w.mu, w.mesh)
+    assert fe.max() <= U.FWD_TOL, (fe.max(), int(ids[fe.argmax()]))
+    lhs = float(np.dot(p.astype(np.float64).ravel(), w.y.astype(np.float64).ravel()))
+    rhs = float(np.dot(w.mu.astype(np.float64), x.astype(np.float64)))
+    assert abs(lhs - rhs) / abs(lhs) <= U.ADJ_TOL
+    _sampled_backprojection_check(tm, w.geom, w.mesh, om, ids, min_nonzero=300)
 
 
 def test_full_size_c5_mesh_sampled():

@@ -316,14 +316,32 @@ def test_orientation_fix_and_validation():
         O.OracleMesh(m.verts, m.tets, bad, m.bfaces)
 
 
-def test_nonconvex_rejected():
-    """Two tets that share only a vertex pair region -> hull not convex."""
+@pytest.mark.parametrize("make", [M.l_shaped_lattice, M.two_disjoint_tets])
+def test_nonconvex_rejected(make):
+    """"The volumetric mesh must be convex" (§2.4).  Both meshes
+    pass every other check (orientation, reciprocity, closed 2-manifold hull),
+    so only the convexity check can reject them -- with code 3.  The L-shape
+    has reflex hull edges; the two disjoint tets have none (each component is
+    convex), so it needs the all-vertices-against-all-hull-planes form."""
+    m = make()
+    with pytest.raises(O.OracleError) as e:
+        O.OracleMesh.from_mesh(m)
+    assert e.value.code == 3, e.value
+    # the same tets minus the offending part are accepted: a convex sub-mesh
+    if make is M.two_disjoint_tets:
+        O.OracleMesh(m.verts[:4], m.tets[:1], m.nbrs[:1], m.bfaces[m.bfaces[:, 0] == 0])
+
+
+def test_carved_lattice_is_non_manifold():
+    """Carving every 7th tet out of a lattice leaves a hull with a repeated
+    directed edge: rejected as a mesh error (code 2) before convexity."""
     a = M.kuhn_lattice(2)
-    keep = [i for i in range(a.n_tets) if i % 7 != 3]   # carve tets -> non-convex
+    keep = [i for i in range(a.n_tets) if i % 7 != 3]
     t = a.tets[keep]
     nb, bf = M.build_graph(t)
-    with pytest.raises(O.OracleError):
+    with pytest.raises(O.OracleError) as e:
         O.OracleMesh(a.verts, t, nb, bf)
+    assert e.value.code == 2, e.value
 
 
 def test_stats_and_crossings_consistent():

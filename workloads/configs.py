@@ -97,11 +97,20 @@ def workload(name: str, n_angles: int | None = None, n_u: int | None = None,
         desc = "Kuhn sliver lattice (aspect 256), lattice-aligned parallel rays"
         sy = 5
     elif name == "c4b":
-        mesh = M.cached(M.jittered_lattice_mesh, 55, 1e-4, 5)
+        n_l, jit = 55, 1e-4
+        mesh = M.cached(M.jittered_lattice_mesh, n_l, jit, 5)
         R = np.sqrt(3.0)
         geom = _scaled_cone(n_angles or 32, 4 * R, 8 * R, 7.2, n_u or 512, n_v or 512)
+        # "sources on lattice points" -- each source moves to
+        # the nearest point of the (unjittered) mesh lattice, extended beyond
+        # the mesh, so rays from it pass within 1e-4 h of lattice vertices
+        h = 2.0 / n_l
+        lo, step = -1 + 2 * jit * h, (2 - 4 * jit * h) / n_l
+        S = geom.vecs[:, 0:3]
+        geom.vecs[:, 0:3] = np.round((lo + np.round((S - lo) / step) * step) * 2.0 ** 22) / 2.0 ** 22
         mu_v = uniform_mu(mesh, 5, 0.5, 1.5)
-        desc = "Delaunay of 1e-4-jittered lattice (slivers), cone 512^2, 32 angles"
+        desc = ("Delaunay of 1e-4-jittered lattice (slivers), cone 512^2, 32 angles, "
+                "sources on lattice points")
         sy = 5
     else:
         raise KeyError(name)

@@ -133,6 +133,24 @@ def kuhn_cube() -> Mesh:
     return kuhn_lattice(1, name="kuhn_cube")
 
 
+def l_shaped_lattice() -> Mesh:
+    """Kuhn lattice(2) minus its (+,+,+) cube: 42 tets whose hull is a closed
+    2-manifold with reflex edges around the removed corner -- a valid graph
+    mesh that violates only the paper's one precondition, "the volumetric
+    mesh must be convex"."""
+    a = kuhn_lattice(2)
+    keep = np.arange(a.n_tets) // 6 != 7          # tet = cube * 6 + permutation
+    return _finish("l_shaped", a.verts, a.tets[keep])
+
+
+def two_disjoint_tets() -> Mesh:
+    """Two separate unit tets: every hull edge is convex (each component is a
+    tetrahedron), so only a global convexity check rejects it."""
+    v = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1],
+                  [3, 0, 0], [4, 0, 0], [3, 1, 0], [3, 0, 1]], dtype=np.float64)
+    return _finish("two_tets", v, np.array([[0, 1, 2, 3], [4, 5, 6, 7]]))
+
+
 # --------------------------------------------------------------------------
 # Delaunay meshes (Qhull through scipy)
 # --------------------------------------------------------------------------
