@@ -401,21 +401,37 @@ typedef struct { int64_t crossings; int lost, stuck, hit; } walk_result;
 /* Alg. 2 for one ray; visit(t, chord) is called for every element crossed. */
 typedef void (*visit_fn)(void* ctx, int32_t t, double chord);
 
-static walk_result walk(const tetref_mesh* m, const int64_t o[3], const int64_t p[3],
-                        visit_fn visit, void* ctx) {
-    walk_result r = {0, 0, 0, 0};
-    /* step 1: entering hull face, by scanning all of them */
+/* Step 1 of Alg. 2: the entering hull face, by scanning all of them
+ * (PAPER.md:146-150).  Returns its tet (-1: the ray misses the mesh) and
+ * sets *kin to the face; more than one entering face marks the ray lost. */
+static int64_t entering_face(const tetref_mesh* m, const int64_t o[3], const int64_t p[3],
+                             walk_result* r, int* kin) {
     int64_t t = -1;
-    int kin = -1, n_enter = 0;
+    int n_enter = 0;
     for (int64_t h = 0; h < m->nb; ++h)
         if (face_crossed(m, m->hull[h][0], m->hull[h][1], o, p, -1)) {
             ++n_enter;
             t = m->hull[h][0];
-            kin = m->hull[h][1];
+            *kin = m->hull[h][1];
         }
-    if (n_enter == 0) return r;          /* "Return if i_now = -1" */
-    if (n_enter > 1) { r.lost = 1; return r; }
-    r.hit = 1;
+    if (n_enter == 0) return -1;
+    if (n_enter > 1) { r->lost = 1; return -1; }
+    r->hit = 1;
+    return t;
+}
+
+static int64_t entering_tet(const tetref_mesh* m, const int64_t o[3], const int64_t p[3],
+                            walk_result* r) {
+    int kin = -1;
+    return entering_face(m, o, p, r, &kin);
+}
+
+static walk_result walk(const tetref_mesh* m, const int64_t o[3], const int64_t p[3],
+                        visit_fn visit, void* ctx) {
+    walk_result r = {0, 0, 0, 0};
+    int kin = -1;
+    int64_t t = entering_face(m, o, p, &r, &kin);
+    if (t < 0) return r;                 /* "Return if i_now = -1" */
     double dx = (double)(p[0] - o[0]), dy = (double)(p[1] - o[1]), dz = (double)(p[2] - o[2]);
     double l = sqrt(dx * dx + dy * dy + dz * dz) * m->g; /* l = |R2-R1| */
     while (t >= 0) {
@@ -548,6 +564,101 @@ int tetref_backproject(const tetref_mesh* m, const tetref_geometry* g, const dou
         st->rays = n_rays; st->rays_hit = hit; st->crossings = cr;
         st->lost = lost; st->stuck = stuck; st->max_crossings = mx;
     }
+    return 0;
+}
+
+/* ------------------------------------------------ NEXT-1: Alg. 1 + Alg. 2 -- */
+#define REAL double
+#define SFX _f64
+#include "tetref_mt.inc"
+#undef REAL
+#undef SFX
+#define REAL float
+#define SFX _f32
+#include "tetref_mt.inc"
+#undef REAL
+#undef SFX
+
+static walk_result mt_walk(const tetref_mesh* m, const int64_t o[3], const int64_t p[3],
+                           const tetref_mt_options* opt, visit_fn visit, void* ctx,
+                           int64_t* esc) {
+    return opt->single ? mt_walk_f32(m, o, p, opt, visit, ctx, esc)
+                       : mt_walk_f64(m, o, p, opt, visit, ctx, esc);
+}
+
+static int check_mt(const tetref_mt_options* opt) {
+    if (!opt || !(opt->eps0 > 0) || !(opt->eps_growth > 1) || opt->max_escalations < 0)
+        return fail(1, "bad MT options");
+    return 0;
+}
+
+static void fill_mt_stats(tetref_mt_stats* st, int64_t n, int64_t hit, int64_t cr, int64_t lost,
+                          int64_t stuck, int64_t mx, int64_t esc) {
+    if (!st) return;
+    st->rays = n; st->rays_hit = hit; st->crossings = cr; st->lost = lost;
+    st->stuck = stuck; st->max_crossings = mx; st->escalations = esc;
+}
+
+int tetref_mt_project(const tetref_mesh* m, const tetref_geometry* g, const double* mu,
+                      int64_t n_rays, const int64_t* ids, double* out,
+                      const tetref_mt_options* opt, int nthreads, tetref_mt_stats* st) {
+    int rc = check_geom(m, g);
+    if (!rc) rc = check_mt(opt);
+    if (rc) return rc;
+    if (!ids) n_rays = (int64_t)g->n_angles * g->n_v * g->n_u;
+    int64_t hit = 0, cr = 0, lost = 0, stuck = 0, mx = 0, bad = 0, esc = 0;
+    int nth = nthreads_of(nthreads);
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nth) \
+    reduction(+ : hit, cr, lost, stuck, bad, esc) reduction(max : mx)
+    for (int64_t i = 0; i < n_rays; ++i) {
+        int64_t o[3], p[3];
+        if (ray_points(m, g, ids ? ids[i] : i, o, p)) { ++bad; continue; }
+        fwd_ctx c = {mu, 0.0};
+        walk_result r = mt_walk(m, o, p, opt, fwd_visit, &c, &esc);
+        out[i] = c.sum;
+        hit += r.hit; cr += r.crossings; lost += r.lost; stuck += r.stuck;
+        if (r.crossings > mx) mx = r.crossings;
+    }
+    if (bad) return fail(4, "ray outside grid span");
+    fill_mt_stats(st, n_rays, hit, cr, lost, stuck, mx, esc);
+    return 0;
+}
+
+int tetref_mt_backproject(const tetref_mesh* m, const tetref_geometry* g, const double* y,
+                          int64_t n_rays, const int64_t* ids, double* x,
+                          const tetref_mt_options* opt, int nthreads, tetref_mt_stats* st) {
+    int rc = check_geom(m, g);
+    if (!rc) rc = check_mt(opt);
+    if (rc) return rc;
+    if (!ids) n_rays = (int64_t)g->n_angles * g->n_v * g->n_u;
+    int nth = nthreads_of(nthreads);
+    while (nth > 1 && (double)nth * m->nt * 8.0 > 4e9) --nth;
+    double* buf = calloc((size_t)nth * m->nt, sizeof(double));
+    if (!buf) return fail(5, "out of memory");
+    int64_t hit = 0, cr = 0, lost = 0, stuck = 0, mx = 0, bad = 0, esc = 0;
+#pragma omp parallel num_threads(nth) reduction(+ : hit, cr, lost, stuck, bad, esc) \
+    reduction(max : mx)
+    {
+        int me = 0;
+#ifdef _OPENMP
+        me = omp_get_thread_num();
+#endif
+        double* mine = buf + (size_t)me * m->nt;
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < n_rays; ++i) {
+            int64_t o[3], p[3];
+            if (ray_points(m, g, ids ? ids[i] : i, o, p)) { ++bad; continue; }
+            bwd_ctx c = {mine, y[i]};
+            walk_result r = mt_walk(m, o, p, opt, bwd_visit, &c, &esc);
+            hit += r.hit; cr += r.crossings; lost += r.lost; stuck += r.stuck;
+            if (r.crossings > mx) mx = r.crossings;
+        }
+    }
+    for (int th = 0; th < nth; ++th)
+        for (int64_t t = 0; t < m->nt; ++t) x[t] += buf[(size_t)th * m->nt + t];
+    free(buf);
+    if (bad) return fail(4, "ray outside grid span");
+    fill_mt_stats(st, n_rays, hit, cr, lost, stuck, mx, esc);
     return 0;
 }
 

@@ -60,6 +60,35 @@ int tetref_ray_points(const tetref_mesh* m, const tetref_geometry* g, int64_t ra
 /* snapped vertex grid coordinates [n_verts][3] */
 int tetref_vertex_grid(const tetref_mesh* m, int64_t* out);
 
+/* ---- NEXT-1: the paper's own traversal (Alg. 1 + Alg. 2) --
+ * eps-guarded Möller-Trumbore with eps escalation, in double (single = 0) or
+ * float (single = 1) on world coordinates; first element = the exact
+ * entering hull tet.  Rays whose escalation exceeds max_escalations are
+ * `lost` (they keep what they summed), walks longer than
+ * 10 ceil(T^(1/3)) + 100 elements are `stuck` (tetref_mt.inc).          */
+typedef struct {
+    int32_t single;            /* 0 = double, 1 = float arithmetic            */
+    int32_t max_escalations;   /* 12 (SPEC.md:314 reading)                    */
+    double eps0;               /* 1e-9 ("eps <- 10^-9")        */
+    double eps_growth;         /* 10   ("eps <- eps * 10")     */
+} tetref_mt_options;
+
+typedef struct {
+    int64_t rays, rays_hit, crossings, lost, stuck, max_crossings, escalations;
+} tetref_mt_stats;
+
+int tetref_mt_project(const tetref_mesh* m, const tetref_geometry* g, const double* mu,
+                      int64_t n_rays, const int64_t* ray_ids, double* out,
+                      const tetref_mt_options* opt, int nthreads, tetref_mt_stats* st);
+int tetref_mt_backproject(const tetref_mesh* m, const tetref_geometry* g, const double* y,
+                          int64_t n_rays, const int64_t* ray_ids, double* x,
+                          const tetref_mt_options* opt, int nthreads, tetref_mt_stats* st);
+/* Alg. 1 alone on one triangle (ray r1 -> r2), in double or float */
+int tetref_mt_hit_f64(const double r1[3], const double r2[3], const double p1[3],
+                      const double p2[3], const double p3[3], double eps, double* t);
+int tetref_mt_hit_f32(const double r1[3], const double r2[3], const double p1[3],
+                      const double p2[3], const double p3[3], double eps, double* t);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,7 +29,7 @@ _native = False
 
 def _stale(lib):
     return not os.path.exists(lib) or os.path.getmtime(lib) < max(
-        os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "tetref.h")))
+        os.path.getmtime(os.path.join(HERE, f)) for f in ("tetref.c", "tetref.h", "tetref_mt.inc"))
 
 
 def build(force: bool = False) -> str:
@@ -73,6 +73,19 @@ class Stats(C.Structure):
         return {k: int(getattr(self, k)) for k, _ in self._fields_}
 
 
+class MtOptions(C.Structure):
+    _fields_ = [("single", C.c_int32), ("max_escalations", C.c_int32), ("eps0", C.c_double),
+                ("eps_growth", C.c_double)]
+
+
+class MtStats(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in
+                ("rays", "rays_hit", "crossings", "lost", "stuck", "max_crossings", "escalations")]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
 _lib = None
 
 
@@ -95,6 +108,11 @@ def lib():
         _lib.tetref_side.argtypes = [P, P, P, P]
         _lib.tetref_ray_points.argtypes = [P, C.POINTER(_Geom), C.c_int64, P, P]
         _lib.tetref_vertex_grid.argtypes = [P, P]
+        for fn in (_lib.tetref_mt_project, _lib.tetref_mt_backproject):
+            fn.argtypes = [P, C.POINTER(_Geom), P, C.c_int64, P, P, C.POINTER(MtOptions), C.c_int,
+                           C.POINTER(MtStats)]
+        for fn in (_lib.tetref_mt_hit_f64, _lib.tetref_mt_hit_f32):
+            fn.argtypes = [P, P, P, P, P, C.c_double, C.POINTER(C.c_double)]
     return _lib
 
 
@@ -210,3 +228,49 @@ def ray_points(mesh: OracleMesh, geom, ray_id: int):
 def side(o, p, a, b) -> int:
     arrs = [np.ascontiguousarray(x, np.int64) for x in (o, p, a, b)]
     return int(lib().tetref_side(*[_ptr(x) for x in arrs]))
+
+
+# ---- NEXT-1: the paper's own traversal (Alg. 1 + Alg. 2), oracle/tetref_mt.inc ----
+def mt_options(single=False, eps0=1e-9, eps_growth=10.0, max_escalations=12):
+    return MtOptions(1 if single else 0, max_escalations, eps0, eps_growth)
+
+
+def mt_project(mesh: OracleMesh, geom, mu, single=False, ray_ids=None, nthreads: int = 0,
+               **kw):
+    """Eq. 2 with the paper's eps-MT traversal in double or float."""
+    g, keep = _geom(geom)
+    mu = np.ascontiguousarray(mu, np.float64)
+    ids = None if ray_ids is None else np.ascontiguousarray(ray_ids, np.int64)
+    out = np.zeros(geom.n_rays if ids is None else len(ids))
+    st = MtStats()
+    opt = mt_options(single, **kw)
+    _check(lib().tetref_mt_project(mesh.h, C.byref(g), _ptr(mu), 0 if ids is None else len(ids),
+                                   None if ids is None else _ptr(ids), _ptr(out), C.byref(opt),
+                                   nthreads, C.byref(st)))
+    if ids is None:
+        out = out.reshape(geom.n_angles, geom.n_v, geom.n_u)
+    return out, st.as_dict()
+
+
+def mt_backproject(mesh: OracleMesh, geom, y, single=False, ray_ids=None, nthreads: int = 0,
+                   **kw):
+    """Eq. 3 with the paper's eps-MT traversal in double or float."""
+    g, keep = _geom(geom)
+    y = np.ascontiguousarray(np.asarray(y, np.float64).ravel())
+    ids = None if ray_ids is None else np.ascontiguousarray(ray_ids, np.int64)
+    x = np.zeros(mesh.n_tets)
+    st = MtStats()
+    opt = mt_options(single, **kw)
+    _check(lib().tetref_mt_backproject(mesh.h, C.byref(g), _ptr(y), 0 if ids is None else len(ids),
+                                       None if ids is None else _ptr(ids), _ptr(x), C.byref(opt),
+                                       nthreads, C.byref(st)))
+    return x, st.as_dict()
+
+
+def mt_hit(r1, r2, p1, p2, p3, eps, single=False):
+    """Alg. 1 on one triangle: (hit, t)."""
+    arrs = [np.ascontiguousarray(a, np.float64) for a in (r1, r2, p1, p2, p3)]
+    t = C.c_double()
+    fn = lib().tetref_mt_hit_f32 if single else lib().tetref_mt_hit_f64
+    hit = fn(*[_ptr(a) for a in arrs], float(eps), C.byref(t))
+    return bool(hit), t.value

@@ -23,6 +23,7 @@ struct tet_mesh {
     HostMesh host;      // keeps grid parameters (arrays freed after upload)
     DevMesh dev;
     void* d_rec = nullptr;
+    void* d_tag16 = nullptr;
     void* d_tnode = nullptr;
     void* d_vtx = nullptr;
     void* d_hull = nullptr;
@@ -491,6 +492,11 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     };
     cudaError_t e = make_pool(device, &m->pool);
     if (e == cudaSuccess) e = up(&m->d_rec, H.rec.data(), H.rec.size() * 4);
+    // FT16 walk unless the mesh exceeds its encoding or TETPROJ_WALKER=rec
+    // asks for the 32-B-record walk (A/B measurements)
+    const char* wk = std::getenv("TETPROJ_WALKER");
+    const bool ft16 = H.ft16 && !(wk && std::string(wk) == "rec");
+    if (e == cudaSuccess && ft16) e = up(&m->d_tag16, H.tag16.data(), H.tag16.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_tnode, H.tnode.data(), H.tnode.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_vtx, H.vtx.data(), H.vtx.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_hull, H.hull.data(), H.hull.size() * 4);
@@ -502,6 +508,7 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
         return cuda_fail(e, "tet_mesh_create upload");
     }
     m->dev.rec = (const int4*)m->d_rec;
+    m->dev.tag16 = (const int4*)m->d_tag16;
     m->dev.tnode = (const int4*)m->d_tnode;
     m->dev.vtx = (const int4*)m->d_vtx;
     m->dev.hull = (const int2*)m->d_hull;
@@ -531,6 +538,7 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     }
     // host copies are no longer needed
     std::vector<int32_t>().swap(H.rec);
+    std::vector<int32_t>().swap(H.tag16);
     std::vector<int32_t>().swap(H.tnode);
     std::vector<int32_t>().swap(H.vtx);
     std::vector<int32_t>().swap(H.hull);
@@ -551,6 +559,7 @@ tet_status tet_mesh_destroy(tet_mesh_t m) {
     for (auto e : m->spare) cudaEventDestroy(e);
     for (auto st : m->streams) cudaStreamDestroy(st);
     cudaFree(m->d_rec);
+    cudaFree(m->d_tag16);
     cudaFree(m->d_tnode);
     cudaFree(m->d_vtx);
     cudaFree(m->d_hull);

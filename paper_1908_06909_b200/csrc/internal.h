@@ -36,6 +36,8 @@ struct HostMesh {
     double g = 0, C[3] = {0, 0, 0};
     std::vector<int32_t> vtx;  // [V][4] grid coords (x,y,z,0), internal vertex order
     std::vector<int32_t> rec;  // [T][8] four face tags (lo, hi) -- see mesh_host.cpp
+    std::vector<int32_t> tag16;// [T][16] four 16-B tags with apex coordinates (FT16 walk)
+    bool ft16 = false;         // the mesh fits the FT16 tag encoding
     std::vector<int32_t> tnode;// [T][4] vertex ids (ray initialisation, entry finder)
     std::vector<int32_t> hull; // [B][2] (t, k) internal order
     std::vector<int32_t> perm; // [T] internal -> caller tet index
@@ -60,6 +62,7 @@ tet_status prepare_geometry(const HostMesh& m, const tet_geometry* g,
 // ------------------------------------------------------------- device ----
 struct DevMesh {
     const int4* rec = nullptr;   // [2T] face tags
+    const int4* tag16 = nullptr; // [4T] FT16 face tags (nullptr: rec walk)
     const int4* tnode = nullptr; // [T] node ids
     const int4* vtx = nullptr;   // [V]
     const int2* hull = nullptr;  // [B]

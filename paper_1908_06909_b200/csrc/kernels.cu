@@ -1046,7 +1046,131 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
         if (!BACK) sum *= ray_scale<UNI>(F, U, g);
     }
 
-template <bool BACK, int BX, int BY, int MINB, bool LATE, bool BAND>
+// ---- FT16 walk: one dependent 16-B gather per step --------------------
+// The tag of the exit face (mesh_host.cpp "FT16") carries the next tet, its
+// apex vertex id AND the apex coordinates, so a step gathers one 16-B tag
+// (plus mu in the forward walk) instead of a 32-B record and a 16-B vertex.
+// Coordinates arrive scaled by 64 (the low 6 bits of each word carry apex-id
+// bits), so this walk runs its shear frame in units of g/64: ray points and
+// vertices x64, tau x4096, chord scale /64 (exact power-of-two scaling: every
+// sign and rounding is that of the unscaled arithmetic).
+constexpr int kFtShift = 6;
+constexpr unsigned kFtHull = 0x3FFFFFFu;
+
+__device__ __forceinline__ int4 ft_scaled(const int4 v) {
+    return make_int4(v.x << kFtShift, v.y << kFtShift, v.z << kFtShift, 0);
+}
+
+__device__ __forceinline__ RayPts ft_scaled(RayPts r) {
+    r.ox <<= kFtShift; r.oy <<= kFtShift; r.oz <<= kFtShift;
+    r.px <<= kFtShift; r.py <<= kFtShift; r.pz <<= kFtShift;
+    return r;
+}
+
+template <bool BACK, int AX, int UNI, int BX, int BY, bool BAND>
+__device__ __forceinline__ void walk_ray_ft(const UniFrame& U, const int4* __restrict__ tag,
+                                            const int4* __restrict__ tnode,
+                                            const int4* __restrict__ vtx,
+                                            const AngleGeom* __restrict__ ang, int beam, int a,
+                                            int u, int v, int nu, int tw_log, double rmax,
+                                            double g, int max_steps, int nverts, int e,
+                                            size_t rid, const float* __restrict__ mu,
+                                            const float* __restrict__ y,
+                                            double* __restrict__ acc, double& sum,
+                                            unsigned& n_cross, unsigned& n_exact,
+                                            unsigned& n_lost, unsigned& n_stuck) {
+    const RayPts r = ft_scaled(ray_points(ang[a], beam, u, v));
+    const double gs = g * (1.0 / (1 << kFtShift));
+    Frame F;
+    if constexpr (UNI == 0) make_frame_ax<AX>(r, rmax * (1 << kFtShift), gs, F);
+    else make_frame_uni<AX, UNI>(r, U, F);
+#if TRACE_BWD_WY32
+    const float wy = BACK ? (float)((double)y[rid] * ray_scale<UNI>(F, U, gs)) : 0.f;
+#else
+    const double wy = BACK ? (double)y[rid] * ray_scale<UNI>(F, U, gs) : 0.0;
+#endif
+    const double tau = UNI ? U.tau : F.tau;
+    const int t0 = e >> 2, kin = e & 3;
+    int t = t0;
+    DBG_CHECK(t >= 0 && t < max_steps);
+    const int4 nodes = __ldg(tnode + t);
+    int id0, id1, id2;
+    if (kin == 0)      { id0 = nodes.y; id1 = nodes.z; id2 = nodes.w; }
+    else if (kin == 1) { id0 = nodes.x; id1 = nodes.w; id2 = nodes.z; }
+    else if (kin == 2) { id0 = nodes.x; id1 = nodes.y; id2 = nodes.w; }
+    else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; }
+    int iap = sel4(nodes, kin);
+    double x0, y0, z0, x1, y1, z1, x2, y2, z2;
+    xf<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id0)), x0, y0, z0);
+    xf<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id1)), x1, y1, z1);
+    xf<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id2)), x2, y2, z2);
+    unsigned n_exact_init = 0;
+    double zin = face_depth(x0, y0, z0, x1, y1, z1, x2, y2, z2, (z0 + z1 + z2) * (1.0 / 3.0),
+                            n_exact_init);
+    int steps = 0;
+    float mut = 0.f;
+    if (!BACK) mut = __ldg(mu + t);
+    int4 X = ft_scaled(__ldg(vtx + iap));                   // apex of the entry tet
+    while (true) {
+        double x3, y3, z3;
+        xf<AX, UNI>(F, U, X, x3, y3, z3);
+        const double p0 = side2(x3, y3, x0, y0);   // side(apex, slot k)
+        const double p1 = side2(x3, y3, x1, y1);
+        const double p2 = side2(x3, y3, x2, y2);
+        unsigned neg = ((unsigned)__double2hiint(p0) >> 31) |
+                       (((unsigned)__double2hiint(p1) >> 30) & 2u) |
+                       (((unsigned)__double2hiint(p2) >> 29) & 4u);
+        if (any_abs_le(p0, p1, p2, tau)) {
+            const unsigned mask = (fabs(p0) <= tau ? 1u : 0u) | (fabs(p1) <= tau ? 2u : 0u) |
+                                  (fabs(p2) <= tau ? 4u : 0u);
+            if (BACK ? TRACE_BWD_ONECALL : TRACE_EXACT_ONECALL) {
+                neg = exact_neg_here<BX, BY, BAND>(vtx, ang, beam, nu, tw_log, mask, neg, iap, id0, id1, id2);
+            } else {
+                const unsigned m = neg;
+                neg = 0;
+                neg |= (mask & 1u) ? (exact_side_here<BX, BY, BAND>(vtx, ang, beam, nu, tw_log, iap, id0) < 0 ? 1u : 0u) : (m & 1u);
+                neg |= (mask & 2u) ? (exact_side_here<BX, BY, BAND>(vtx, ang, beam, nu, tw_log, iap, id1) < 0 ? 2u : 0u) : (m & 2u);
+                neg |= (mask & 4u) ? (exact_side_here<BX, BY, BAND>(vtx, ang, beam, nu, tw_log, iap, id2) < 0 ? 4u : 0u) : (m & 4u);
+            }
+            n_exact += __popc(mask);
+        }
+        const int j = (int)((kExitLUT >> (2 * neg)) & 3u);
+        const int idj = selp(id0, selp(id1, id2, j == 1), j == 0);
+        const int L = rank4(id0, id1, id2, iap, idj);
+        // the exit face's tag: issued now, consumed after this step's chord
+        const int4 tg = __ldg(tag + 4 * (size_t)t + (j == 3 ? 0 : L));
+        const int tcur = t;
+        if (j == 0) { x0 = x3; y0 = y3; z0 = z3; id0 = iap; }
+        if (j == 1) { x1 = x3; y1 = y3; z1 = z3; id1 = iap; }
+        if (j == 2) { x2 = x3; y2 = y3; z2 = z3; id2 = iap; }
+        const double zout = face_depth(x0, y0, z0, x1, y1, z1, x2, y2, z2, zin, n_exact);
+        const double dz = zout - zin;
+        if (BACK) {
+            if (dz > 0.0) atomicAdd(acc + tcur, dz * f2d_here(wy));
+        } else {
+            sum = fma(dz, (double)mut, sum);
+        }
+        const unsigned n26 = (unsigned)tg.w & kFtHull;
+        const bool more = n26 != kFtHull && j != 3 && ++steps != max_steps;
+        if (!more) {
+            const bool stuck = n26 != kFtHull && j != 3;
+            n_lost += j == 3 ? 1u : 0u;
+            n_stuck += stuck ? 1u : 0u;
+            n_cross += (unsigned)steps + (stuck ? 0u : 1u);
+            break;
+        }
+        t = (int)n26;
+        if (!BACK) mut = __ldg(mu + t);
+        X = make_int4(tg.x & ~63, tg.y & ~63, tg.z & ~63, 0);
+        iap = (int)(((unsigned)tg.w >> 26) | (((unsigned)tg.x & 63u) << 6) |
+                    (((unsigned)tg.y & 63u) << 12) | (((unsigned)tg.z & 63u) << 18));
+        DBG_CHECK(t >= 0 && t < max_steps && iap >= 0 && iap < nverts);
+        zin = zout;
+    }
+    if (!BACK) sum *= ray_scale<UNI>(F, U, gs);
+}
+
+template <bool BACK, int BX, int BY, int MINB, bool LATE, bool BAND, bool FT>
 __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* __restrict__ rec,
                                                           const int4* __restrict__ tnode,
                                                           const int4* __restrict__ vtx,
@@ -1111,10 +1235,13 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
     }
     const UniFrame& U = UF.f[a];
     if (e >= 0) {
-#define WALK(AXV, UNI) walk_ray<BACK, AXV, UNI, BX, BY, LATE, BAND>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tile_code, rmax, g, \
+#define WALK(AXV, UNI) do { \
+    if (FT) walk_ray_ft<BACK, AXV, UNI, BX, BY, BAND>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tile_code, rmax, g, \
+                                      max_steps, nverts, e, rid, mu, y, acc, sum, n_cross, n_exact, n_lost, n_stuck); \
+    else walk_ray<BACK, AXV, UNI, BX, BY, LATE, BAND>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tile_code, rmax, g, \
                                       max_steps, \
                                       nverts, e, rid, mu, y, acc, sum, n_cross, n_exact, n_lost, \
-                                      n_stuck)
+                                      n_stuck); } while (0)
         // uniform frames (TRACE_BWD_UNI = 0: per-ray frame in the backward walk)
         // (one kernel per beam type spills the forward walk's frame: the
         // register allocation of this combined kernel is the measured best)
@@ -1160,24 +1287,51 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
 // coordinates.  The first tet comes from the exact entry map (the paper's
 // R*-tree initialisation is replaced); everything after it is
 // the paper's method, including its failure modes.
+// Single IEEE operations (never contracted into FMAs) in the order Alg. 1
+// writes them, so the MT modes compute exactly what IEEE arithmetic in T
+// computes for the paper's algorithm -- the single-precision failures of
+// fig:singledouble are then reproducible operation for operation.
+__device__ __forceinline__ double o_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double o_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double o_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double o_div(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double o_sqrt(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ float o_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float o_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float o_sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float o_div(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float o_sqrt(float a) { return __fsqrt_rn(a); }
+
+template <class T>
+__device__ __forceinline__ T o_dot(const T a[3], const T b[3]) {
+    return o_add(o_add(o_mul(a[0], b[0]), o_mul(a[1], b[1])), o_mul(a[2], b[2]));
+}
+
+template <class T>
+__device__ __forceinline__ void o_cross(const T a[3], const T b[3], T c[3]) {
+    c[0] = o_sub(o_mul(a[1], b[2]), o_mul(a[2], b[1]));
+    c[1] = o_sub(o_mul(a[2], b[0]), o_mul(a[0], b[2]));
+    c[2] = o_sub(o_mul(a[0], b[1]), o_mul(a[1], b[0]));
+}
+
 template <class T>
 __device__ __forceinline__ bool mt_hit(const T r1[3], const T d[3], const T p1[3], const T p2[3],
                                        const T p3[3], T eps, T& t) {
-    const T e1[3] = {p2[0] - p1[0], p2[1] - p1[1], p2[2] - p1[2]};
-    const T e2[3] = {p3[0] - p1[0], p3[1] - p1[1], p3[2] - p1[2]};
-    const T q[3] = {d[1] * e2[2] - d[2] * e2[1], d[2] * e2[0] - d[0] * e2[2],
-                    d[0] * e2[1] - d[1] * e2[0]};
-    const T a = e1[0] * q[0] + e1[1] * q[1] + e1[2] * q[2];
+    const T e1[3] = {o_sub(p2[0], p1[0]), o_sub(p2[1], p1[1]), o_sub(p2[2], p1[2])};
+    const T e2[3] = {o_sub(p3[0], p1[0]), o_sub(p3[1], p1[1]), o_sub(p3[2], p1[2])};
+    T q[3];
+    o_cross(d, e2, q);                                         // q = d x E2
+    const T a = o_dot(e1, q);
     if (a > T(-1e-8) && a < T(1e-8)) return false;            // "Check if its zero"
-    const T f = T(1) / a;
-    const T s[3] = {r1[0] - p1[0], r1[1] - p1[1], r1[2] - p1[2]};
-    const T u = f * (s[0] * q[0] + s[1] * q[1] + s[2] * q[2]);
+    const T f = o_div(T(1), a);
+    const T s[3] = {o_sub(r1[0], p1[0]), o_sub(r1[1], p1[1]), o_sub(r1[2], p1[2])};
+    const T u = o_mul(f, o_dot(s, q));
     if (u < -eps) return false;
-    const T r[3] = {s[1] * e1[2] - s[2] * e1[1], s[2] * e1[0] - s[0] * e1[2],
-                    s[0] * e1[1] - s[1] * e1[0]};
-    const T v = f * (d[0] * r[0] + d[1] * r[1] + d[2] * r[2]);   // printed "d x r": a dot (R2 reading)
-    if (v < -eps || u + v > T(1) + eps) return false;
-    t = f * (e2[0] * r[0] + e2[1] * r[1] + e2[2] * r[2]);
+    T r[3];
+    o_cross(s, e1, r);                                         // r = s x E1
+    const T v = o_mul(f, o_dot(d, r));   // printed "d x r": a dot (R2 reading)
+    if (v < -eps || o_add(u, v) > o_add(T(1), eps)) return false;
+    t = o_mul(f, o_dot(e2, r));
     return true;
 }
 
@@ -1225,8 +1379,8 @@ __global__ void __launch_bounds__(128) mt_trace_kernel(const int4* __restrict__ 
                                fma((double)rp.pz, g, C[2])};
         const T R1[3] = {(T)R1d[0], (T)R1d[1], (T)R1d[2]};
         const T R2[3] = {(T)R2d[0], (T)R2d[1], (T)R2d[2]};
-        const T d[3] = {R2[0] - R1[0], R2[1] - R1[1], R2[2] - R1[2]};
-        const T l = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);   // l = ||R2 - R1||
+        const T d[3] = {o_sub(R2[0], R1[0]), o_sub(R2[1], R1[1]), o_sub(R2[2], R1[2])};
+        const T l = o_sqrt(o_dot(d, d));                             // l = ||R2 - R1||
         const float yv = BACK ? y[rid] : 0.f;
         int t = e >> 2, prev = -1;
         int steps = 0;
@@ -1246,22 +1400,25 @@ __global__ void __launch_bounds__(128) mt_trace_kernel(const int4* __restrict__ 
                     const int i0 = k == 0 ? 1 : 0, i1 = k <= 1 ? 2 : 1, i2 = k <= 2 ? 3 : 2;
                     T th;
                     if (mt_hit<T>(R1, d, P[i0], P[i1], P[i2], eps, th)) {
+                        // t1: the first face with the minimal t; t2: the last
+                        // with the maximal t -- two hits at equal t come out
+                        // in encounter order (R16)
                         if (nhit == 0 || th < tmin) { tmin = th; kmin = k; }
-                        if (nhit == 0 || th > tmax) { tmax = th; kmax = k; }
+                        if (nhit == 0 || th >= tmax) { tmax = th; kmax = k; }
                         ++nhit;
                     }
                 }
                 if (nhit >= 2 || esc >= max_esc) break;
-                eps = eps * (T)eps_growth;
+                eps = o_mul(eps, (T)eps_growth);
                 ++esc;
             }
             n_esc += esc;
             if (nhit < 2) { ++n_lost; break; }                // the "black dots"
-            const double chord = (double)(l * (tmax - tmin));
+            const double chord = (double)o_mul(l, o_sub(tmax, tmin));   // l (t2 - t1)
             if (BACK) {
                 if (chord > 0.0) atomicAdd(acc + t, chord * (double)yv);
             } else {
-                sum = fma(chord, (double)__ldg(mu + t), sum);
+                sum = o_add(sum, o_mul(chord, (double)__ldg(mu + t)));
             }
             ++n_cross;
             // neighbour of the face where t2 happened; "if t2 = t1 check if they
@@ -1406,7 +1563,7 @@ static dim3 trace_grid_w(const LaunchChunk& c, int tw_log, int bx, int by) {
     return dim3(tiles, (unsigned)c.n_angles);
 }
 
-#define TRACE_ARGS m.rec, m.tnode, m.vtx, c.ang, c.beam, c.nv, c.nu, m.rmax, m.g, steps, entry, \
+#define TRACE_ARGS rec_or_tag, m.tnode, m.vtx, c.ang, c.beam, c.nv, c.nu, m.rmax, m.g, steps, entry, \
                    mu_int, proj, y, acc, stats
 
 // Walker block shape (BX x BY warp tiles) and the blocks per SM it is compiled
@@ -1452,19 +1609,20 @@ template <> struct TraceShape<true, true> {
     static constexpr bool LATE = false;
 };
 
-// Host half of make_frame_uni: the block-uniform frame of each angle.
-static void make_uni_frames(const DevMesh& m, const LaunchChunk& c, UniFrames& U) {
+// Host half of make_frame_uni: the block-uniform frame of each angle, in
+// grid units / `sc` (sc = 64 for the FT16 walk, whose coordinates are x64).
+static void make_uni_frames(const DevMesh& m, const LaunchChunk& c, UniFrames& U, double sc) {
     for (int a = 0; a < c.n_angles; ++a) {
         const AngleGeom& G = c.host_ang[a];
         UniFrame& f = U.f[a];
         if (c.beam == TET_BEAM_CONE) {
             double n2 = 0;
             for (int i = 0; i < 3; ++i) {
-                f.q[i] = (double)G.o[i];
+                f.q[i] = (double)G.o[i] * sc;
                 n2 += f.q[i] * f.q[i];
             }
             // |X - S| <= |S| + rmax;  (1 + |sx| + |sy|) / 2 <= 2.5
-            const double amax = (std::sqrt(n2) + m.rmax) * 2.5;
+            const double amax = (std::sqrt(n2) + m.rmax * sc) * 2.5;
             f.tau = amax * amax * 0x1p-38;
             f.scale = 0;
         } else {
@@ -1491,10 +1649,10 @@ static void make_uni_frames(const DevMesh& m, const LaunchChunk& c, UniFrames& U
                     }
                     omax = std::max(omax, std::sqrt(n2));
                 }
-            const double amax = (omax + m.rmax) * (1.0 + std::fabs(f.q[0]) + std::fabs(f.q[1])) * 0.5;
+            const double amax = (omax + m.rmax) * sc * (1.0 + std::fabs(f.q[0]) + std::fabs(f.q[1])) * 0.5;
             f.tau = amax * amax * 0x1p-38;
             const double dx = (double)d[0], dy = (double)d[1], dz = (double)d[2];
-            f.scale = std::sqrt(dx * dx + dy * dy + dz * dz) / adk * m.g;
+            f.scale = std::sqrt(dx * dx + dy * dy + dz * dz) / adk * (m.g / sc);
         }
     }
 }
@@ -1516,9 +1674,13 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     const int group = big ? (BACK ? TRACE_BWD_BAND_GROUP : 1 << 20) : 0;
     const int tile_code = twl | group << 4;
     static thread_local UniFrames U;   // 10 KB: copied into the launch parameters
-    make_uni_frames(m, c, U);
-    auto kern = big ? trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, true>
-                    : trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, false>;
+    const bool ft = m.tag16 != nullptr;   // FT16 walk (coordinates x64)
+    make_uni_frames(m, c, U, ft ? (double)(1 << kFtShift) : 1.0);
+    auto kern = ft ? (big ? trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, true, true>
+                          : trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, false, true>)
+                   : (big ? trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, true, false>
+                          : trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, false, false>);
+    const int4* rec_or_tag = ft ? m.tag16 : m.rec;
     if (m.l2_window_bytes == 0) {
         kern<<<trace_grid_w(c, twl, S::BX, S::BY), 32 * S::BX * S::BY, 0, s>>>(TRACE_ARGS, tile_code,
                                                                                (int)m.nv, U);

@@ -409,6 +409,42 @@ tet_status prepare_mesh(const double* verts, int64_t nv, const int32_t* tets,
             M.rec[8 * i + 2 * r + 1] = vnew[T[4 * (int64_t)n + kp]];
         }
     }
+    // 16-B face tags carrying the next apex's COORDINATES (DESIGN.md §5,
+    // "FT16 walk"): tag r of tet i (same rank order as rec) packs
+    //   w3 = n (26 bits; 2^26 - 1 on the hull) | apex id bits 0..5 << 26
+    //   w0 = X << 6 | apex id bits 6..11,  w1 = Y << 6 | bits 12..17,
+    //   w2 = Z << 6 | bits 18..23
+    // (X, Y, Z = the apex's grid coordinates, |.| <= 2^24 + 1 < 2^25 by the
+    // numeric contract), so the walker learns the next tet, its apex id AND
+    // the apex position from one 16-B load -- no vertex gather in the loop.
+    // Meshes with >= 2^26 - 1 tets or >= 2^24 vertices keep the rec walk.
+    M.ft16 = nt < (1 << 26) - 1 && nvu < (1 << 24);
+    if (M.ft16) {
+        M.tag16.assign((size_t)nt * 16, 0);
+        for (int64_t i = 0; i < nt; ++i) {
+            const int64_t t = order[i];
+            int32_t ids[4];
+            for (int k = 0; k < 4; ++k) ids[k] = vnew[T[4 * t + k]];
+            for (int k = 0; k < 4; ++k) {
+                int r = 0;
+                for (int j = 0; j < 4; ++j) r += ids[j] < ids[k];
+                const int32_t n = N[4 * t + k];
+                uint32_t n26 = 0x3FFFFFFu, apex = 0;
+                int32_t X[3] = {0, 0, 0};
+                if (n >= 0) {
+                    const int32_t va = T[4 * (int64_t)n + kback[4 * t + k]];
+                    n26 = (uint32_t)inv[n];
+                    apex = (uint32_t)vnew[va];
+                    for (int c = 0; c < 3; ++c) X[c] = P[3 * (int64_t)va + c];
+                }
+                uint32_t* w = reinterpret_cast<uint32_t*>(&M.tag16[16 * i + 4 * r]);
+                w[0] = ((uint32_t)X[0] << 6) | ((apex >> 6) & 63u);
+                w[1] = ((uint32_t)X[1] << 6) | ((apex >> 12) & 63u);
+                w[2] = ((uint32_t)X[2] << 6) | ((apex >> 18) & 63u);
+                w[3] = n26 | ((apex & 63u) << 26);
+            }
+        }
+    }
     M.hull.resize((size_t)B * 2);
     for (int64_t h = 0; h < B; ++h) {
         M.hull[2 * h] = inv[hull[h].first];
