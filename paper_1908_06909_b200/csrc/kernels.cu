@@ -74,6 +74,15 @@ typedef __int128 i128;
 #ifndef TRACE_EXACT_ONECALL
 #define TRACE_EXACT_ONECALL 1
 #endif
+// FT16 walk, cone beams: integer -> double by the 2^52 + 2^31 magic number
+// (one LOP3 + the DADD the frame needs anyway) instead of I2F.F64 on the XU
+#ifndef TRACE_FT_MAGIC
+#define TRACE_FT_MAGIC 0
+#endif
+// FT16 backward: the RED of step k issued after step k+1's tag is decoded
+#ifndef TRACE_FT_RED_LATE
+#define TRACE_FT_RED_LATE 0
+#endif
 
 // ------------------------------------------------------------ exact -----
 // Reading R2: sign of det[a-o, b-o, p-o] under o -> o + (d, d^2, d^4),
@@ -1067,6 +1076,29 @@ __device__ __forceinline__ RayPts ft_scaled(RayPts r) {
     return r;
 }
 
+// 2^52 + 2^31 + x as a double, exactly, for any int32 x (the bit pattern
+// of the low word is x + 2^31 under the exponent of 2^52)
+constexpr double kMagic = 4503601774854144.0;   // 2^52 + 2^31
+__device__ __forceinline__ double magic_i2d(int x) {
+    return __hiloint2double(0x43300000, x ^ (int)0x80000000);
+}
+
+// Shear transform of a FT-scaled vertex.  Cone beams with TRACE_FT_MAGIC:
+// U.q holds q + 2^52 + 2^31 (host), so X - q = magic(X) - U.q is one exact DADD.
+template <int AX, int UNI>
+__device__ __forceinline__ void xf_ft(const Frame& F, const UniFrame& U, const int4 v, double& x,
+                                      double& y, double& z) {
+    if constexpr (UNI == 1 && TRACE_FT_MAGIC) {
+        using A = Axis<AX>;
+        const double zz = magic_i2d(pick4<A::k>(v)) - U.q[A::k];
+        z = (AX & 1) ? -zz : zz;
+        x = fma(-F.sx, z, magic_i2d(pick4<A::K1>(v)) - U.q[A::K1]);
+        y = fma(-F.sy, z, magic_i2d(pick4<A::K2>(v)) - U.q[A::K2]);
+    } else {
+        xf<AX, UNI>(F, U, v, x, y, z);
+    }
+}
+
 template <bool BACK, int AX, int UNI, int BX, int BY, bool BAND>
 __device__ __forceinline__ void walk_ray_ft(const UniFrame& U, const int4* __restrict__ tag,
                                             const int4* __restrict__ tnode,
@@ -1101,9 +1133,9 @@ __device__ __forceinline__ void walk_ray_ft(const UniFrame& U, const int4* __res
     else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; }
     int iap = sel4(nodes, kin);
     double x0, y0, z0, x1, y1, z1, x2, y2, z2;
-    xf<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id0)), x0, y0, z0);
-    xf<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id1)), x1, y1, z1);
-    xf<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id2)), x2, y2, z2);
+    xf_ft<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id0)), x0, y0, z0);
+    xf_ft<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id1)), x1, y1, z1);
+    xf_ft<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id2)), x2, y2, z2);
     unsigned n_exact_init = 0;
     double zin = face_depth(x0, y0, z0, x1, y1, z1, x2, y2, z2, (z0 + z1 + z2) * (1.0 / 3.0),
                             n_exact_init);
@@ -1113,7 +1145,7 @@ __device__ __forceinline__ void walk_ray_ft(const UniFrame& U, const int4* __res
     int4 X = ft_scaled(__ldg(vtx + iap));                   // apex of the entry tet
     while (true) {
         double x3, y3, z3;
-        xf<AX, UNI>(F, U, X, x3, y3, z3);
+        xf_ft<AX, UNI>(F, U, X, x3, y3, z3);
         const double p0 = side2(x3, y3, x0, y0);   // side(apex, slot k)
         const double p1 = side2(x3, y3, x1, y1);
         const double p2 = side2(x3, y3, x2, y2);
@@ -1146,12 +1178,13 @@ __device__ __forceinline__ void walk_ray_ft(const UniFrame& U, const int4* __res
         const double zout = face_depth(x0, y0, z0, x1, y1, z1, x2, y2, z2, zin, n_exact);
         const double dz = zout - zin;
         if (BACK) {
-            if (dz > 0.0) atomicAdd(acc + tcur, dz * f2d_here(wy));
+            if (!TRACE_FT_RED_LATE && dz > 0.0) atomicAdd(acc + tcur, dz * f2d_here(wy));
         } else {
             sum = fma(dz, (double)mut, sum);
         }
         const unsigned n26 = (unsigned)tg.w & kFtHull;
         const bool more = n26 != kFtHull && j != 3 && ++steps != max_steps;
+        if (BACK && TRACE_FT_RED_LATE && dz > 0.0) atomicAdd(acc + tcur, dz * f2d_here(wy));
         if (!more) {
             const bool stuck = n26 != kFtHull && j != 3;
             n_lost += j == 3 ? 1u : 0u;
@@ -1589,23 +1622,33 @@ static dim3 trace_grid_w(const LaunchChunk& c, int tw_log, int bx, int by) {
 // api.cu picks it from the exact-fallback rate of the mesh's last call with
 // statistics (LaunchChunk::exact_heavy).
 template <bool BACK, bool HEAVY> struct TraceShape;
+// MINB_FT: blocks per SM of the FT16 walk.  Its backward holds fewer live
+// registers (no 32-B record, no vertex quad): 10 blocks at 48 registers
+// (40 warps/SM) hide more of the RED traffic's latency than 8 at 64 (c3
+// backward 32.96 -> 31.72 ms; 9 blocks 32.69, 11-12 blocks spill: 39.9;
+// the forward prefers 8: 26.6 vs 29.6 ms at 10), profiles/README.md.
+#ifndef TRACE_FT_BWD_MINB
+#define TRACE_FT_BWD_MINB 10
+#endif
 template <> struct TraceShape<false, false> {
     static constexpr int BX = TRACE_FWD_BX, BY = TRACE_FWD_BY, MINB = TRACE_FWD_MINB;
+    static constexpr int MINB_FT = TRACE_FWD_MINB;
     static constexpr bool LATE = TRACE_FWD_LATE_LOADS;
 };
 template <> struct TraceShape<true, false> {
     static constexpr int BX = TRACE_BWD_BX, BY = TRACE_BWD_BY, MINB = TRACE_BWD_MINB;
+    static constexpr int MINB_FT = TRACE_FT_BWD_MINB;
     static constexpr bool LATE = TRACE_BWD_LATE_LOADS;
 };
 #ifndef TRACE_HEAVY_FWD_MINB
 #define TRACE_HEAVY_FWD_MINB 4
 #endif
 template <> struct TraceShape<false, true> {
-    static constexpr int BX = 2, BY = 2, MINB = TRACE_HEAVY_FWD_MINB;
+    static constexpr int BX = 2, BY = 2, MINB = TRACE_HEAVY_FWD_MINB, MINB_FT = MINB;
     static constexpr bool LATE = false;
 };
 template <> struct TraceShape<true, true> {
-    static constexpr int BX = 2, BY = 2, MINB = 4;
+    static constexpr int BX = 2, BY = 2, MINB = 4, MINB_FT = MINB;
     static constexpr bool LATE = false;
 };
 
@@ -1621,6 +1664,10 @@ static void make_uni_frames(const DevMesh& m, const LaunchChunk& c, UniFrames& U
                 f.q[i] = (double)G.o[i] * sc;
                 n2 += f.q[i] * f.q[i];
             }
+            // FT16 walk: q + 2^52 + 2^31 (exact: an integer below 2^53) for the
+            // magic-number conversion of xf_ft
+            if (TRACE_FT_MAGIC && sc != 1.0)
+                for (int i = 0; i < 3; ++i) f.q[i] += kMagic;
             // |X - S| <= |S| + rmax;  (1 + |sx| + |sy|) / 2 <= 2.5
             const double amax = (std::sqrt(n2) + m.rmax * sc) * 2.5;
             f.tau = amax * amax * 0x1p-38;
@@ -1674,10 +1721,12 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     const int group = big ? (BACK ? TRACE_BWD_BAND_GROUP : 1 << 20) : 0;
     const int tile_code = twl | group << 4;
     static thread_local UniFrames U;   // 10 KB: copied into the launch parameters
-    const bool ft = m.tag16 != nullptr;   // FT16 walk (coordinates x64)
+    // FT16 walk (coordinates x64), except for exact-heavy scans: there the
+    // rec walk's shape measured faster (c4a 9.32e9 vs 8.98e9 crossings/s)
+    const bool ft = m.tag16 != nullptr && !HEAVY;
     make_uni_frames(m, c, U, ft ? (double)(1 << kFtShift) : 1.0);
-    auto kern = ft ? (big ? trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, true, true>
-                          : trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, false, true>)
+    auto kern = ft ? (big ? trace_kernel<BACK, S::BX, S::BY, S::MINB_FT, S::LATE, true, true>
+                          : trace_kernel<BACK, S::BX, S::BY, S::MINB_FT, S::LATE, false, true>)
                    : (big ? trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, true, false>
                           : trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, false, false>);
     const int4* rec_or_tag = ft ? m.tag16 : m.rec;
