@@ -74,15 +74,7 @@ typedef __int128 i128;
 #ifndef TRACE_EXACT_ONECALL
 #define TRACE_EXACT_ONECALL 1
 #endif
-// FT16 walk, cone beams: integer -> double by the 2^52 + 2^31 magic number
-// (one LOP3 + the DADD the frame needs anyway) instead of I2F.F64 on the XU
-#ifndef TRACE_FT_MAGIC
-#define TRACE_FT_MAGIC 0
-#endif
-// FT16 backward: the RED of step k issued after step k+1's tag is decoded
-#ifndef TRACE_FT_RED_LATE
-#define TRACE_FT_RED_LATE 0
-#endif
+
 
 // ------------------------------------------------------------ exact -----
 // Reading R2: sign of det[a-o, b-o, p-o] under o -> o + (d, d^2, d^4),
@@ -305,11 +297,15 @@ __device__ __forceinline__ int icomp(const int4 v, int k) {
     return selp(v.x, selp(v.y, v.z, k == 1), k == 0);
 }
 
-// reciprocal: MUFU approximation (~2^-23) + one fp64 Newton step (~2^-46)
+// reciprocal: MUFU approximation (~2^-23) + one fp64 Newton step (~2^-46);
+// TRACE_RCP_NEWTON = 0 keeps the bare approximation (A/B knob)
+#ifndef TRACE_RCP_NEWTON
+#define TRACE_RCP_NEWTON 1
+#endif
 __device__ __forceinline__ double rcp_nr(double x) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    return r * fma(-x, r, 2.0);
+    return TRACE_RCP_NEWTON ? r * fma(-x, r, 2.0) : r;
 }
 
 __device__ __forceinline__ void xform(const Frame& F, const int4 v, double& x, double& y,
@@ -1076,29 +1072,6 @@ __device__ __forceinline__ RayPts ft_scaled(RayPts r) {
     return r;
 }
 
-// 2^52 + 2^31 + x as a double, exactly, for any int32 x (the bit pattern
-// of the low word is x + 2^31 under the exponent of 2^52)
-constexpr double kMagic = 4503601774854144.0;   // 2^52 + 2^31
-__device__ __forceinline__ double magic_i2d(int x) {
-    return __hiloint2double(0x43300000, x ^ (int)0x80000000);
-}
-
-// Shear transform of a FT-scaled vertex.  Cone beams with TRACE_FT_MAGIC:
-// U.q holds q + 2^52 + 2^31 (host), so X - q = magic(X) - U.q is one exact DADD.
-template <int AX, int UNI>
-__device__ __forceinline__ void xf_ft(const Frame& F, const UniFrame& U, const int4 v, double& x,
-                                      double& y, double& z) {
-    if constexpr (UNI == 1 && TRACE_FT_MAGIC) {
-        using A = Axis<AX>;
-        const double zz = magic_i2d(pick4<A::k>(v)) - U.q[A::k];
-        z = (AX & 1) ? -zz : zz;
-        x = fma(-F.sx, z, magic_i2d(pick4<A::K1>(v)) - U.q[A::K1]);
-        y = fma(-F.sy, z, magic_i2d(pick4<A::K2>(v)) - U.q[A::K2]);
-    } else {
-        xf<AX, UNI>(F, U, v, x, y, z);
-    }
-}
-
 template <bool BACK, int AX, int UNI, int BX, int BY, bool BAND>
 __device__ __forceinline__ void walk_ray_ft(const UniFrame& U, const int4* __restrict__ tag,
                                             const int4* __restrict__ tnode,
@@ -1133,9 +1106,9 @@ __device__ __forceinline__ void walk_ray_ft(const UniFrame& U, const int4* __res
     else               { id0 = nodes.x; id1 = nodes.z; id2 = nodes.y; }
     int iap = sel4(nodes, kin);
     double x0, y0, z0, x1, y1, z1, x2, y2, z2;
-    xf_ft<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id0)), x0, y0, z0);
-    xf_ft<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id1)), x1, y1, z1);
-    xf_ft<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id2)), x2, y2, z2);
+    xf<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id0)), x0, y0, z0);
+    xf<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id1)), x1, y1, z1);
+    xf<AX, UNI>(F, U, ft_scaled(__ldg(vtx + id2)), x2, y2, z2);
     unsigned n_exact_init = 0;
     double zin = face_depth(x0, y0, z0, x1, y1, z1, x2, y2, z2, (z0 + z1 + z2) * (1.0 / 3.0),
                             n_exact_init);
@@ -1145,7 +1118,7 @@ __device__ __forceinline__ void walk_ray_ft(const UniFrame& U, const int4* __res
     int4 X = ft_scaled(__ldg(vtx + iap));                   // apex of the entry tet
     while (true) {
         double x3, y3, z3;
-        xf_ft<AX, UNI>(F, U, X, x3, y3, z3);
+        xf<AX, UNI>(F, U, X, x3, y3, z3);
         const double p0 = side2(x3, y3, x0, y0);   // side(apex, slot k)
         const double p1 = side2(x3, y3, x1, y1);
         const double p2 = side2(x3, y3, x2, y2);
@@ -1178,13 +1151,12 @@ __device__ __forceinline__ void walk_ray_ft(const UniFrame& U, const int4* __res
         const double zout = face_depth(x0, y0, z0, x1, y1, z1, x2, y2, z2, zin, n_exact);
         const double dz = zout - zin;
         if (BACK) {
-            if (!TRACE_FT_RED_LATE && dz > 0.0) atomicAdd(acc + tcur, dz * f2d_here(wy));
+            if (dz > 0.0) atomicAdd(acc + tcur, dz * f2d_here(wy));
         } else {
             sum = fma(dz, (double)mut, sum);
         }
         const unsigned n26 = (unsigned)tg.w & kFtHull;
         const bool more = n26 != kFtHull && j != 3 && ++steps != max_steps;
-        if (BACK && TRACE_FT_RED_LATE && dz > 0.0) atomicAdd(acc + tcur, dz * f2d_here(wy));
         if (!more) {
             const bool stuck = n26 != kFtHull && j != 3;
             n_lost += j == 3 ? 1u : 0u;
@@ -1664,10 +1636,6 @@ static void make_uni_frames(const DevMesh& m, const LaunchChunk& c, UniFrames& U
                 f.q[i] = (double)G.o[i] * sc;
                 n2 += f.q[i] * f.q[i];
             }
-            // FT16 walk: q + 2^52 + 2^31 (exact: an integer below 2^53) for the
-            // magic-number conversion of xf_ft
-            if (TRACE_FT_MAGIC && sc != 1.0)
-                for (int i = 0; i < 3; ++i) f.q[i] += kMagic;
             // |X - S| <= |S| + rmax;  (1 + |sx| + |sy|) / 2 <= 2.5
             const double amax = (std::sqrt(n2) + m.rmax * sc) * 2.5;
             f.tau = amax * amax * 0x1p-38;
