@@ -1,9 +1,10 @@
 #!/usr/bin/env python
 """NEXT-3: entry finders compared -- per-(face, angle) exact rasterisation of
-hull-face footprints (default) vs a per-ray BVH search over the hull faces
-(the paper's tree-search initialisation).  Both take the
-same exact decision: the projections must be bit-identical.  One JSON line per
-config with the entry-finder milliseconds of one forward projection."""
+hull-face footprints (default) vs per-ray searches of a binary BVH and of the
+paper's R*-tree (fan-out 4..10, depth-first) over the hull
+faces.  All take the same exact decision: the projections must be
+bit-identical.  One JSON line per config with the entry-finder milliseconds
+of one forward projection."""
 import json
 import os
 import sys
@@ -24,7 +25,8 @@ def main():
         tm = T.TetMesh.from_mesh(w.mesh)
         mu = torch.from_numpy(w.mu).cuda()
         res = {}
-        for ename, mode in [("raster", T.TET_ENTRY_RASTER), ("bvh", T.TET_ENTRY_BVH)]:
+        for ename, mode in [("raster", T.TET_ENTRY_RASTER), ("bvh", T.TET_ENTRY_BVH),
+                            ("rtree", T.TET_ENTRY_RTREE)]:
             opts = T.options(entry=mode)
             p, st = tm.project(w.geom, mu, stats=True, opts=opts)
             T.tet_set_kernel_timing(tm.handle, True)
@@ -35,12 +37,13 @@ def main():
             kt = T.tet_kernel_times(tm.handle)
             T.tet_set_kernel_timing(tm.handle, False)
             res[ename] = (p.clone(), st, kt["entry"][0] / 3, kt["forward"][0] / 3)
-        same = bool(torch.equal(res["raster"][0], res["bvh"][0]))
+        same = all(torch.equal(res["raster"][0], res[k][0]) for k in ("bvh", "rtree"))
         line = {"config": name, "tets": w.mesh.n_tets, "hull_faces": w.mesh.n_bfaces,
                 "rays": w.geom.n_rays, "identical": same,
                 "raster_entry_ms": res["raster"][2], "bvh_entry_ms": res["bvh"][2],
-                "walk_ms": res["raster"][3],
-                "crossings_equal": res["raster"][1]["crossings"] == res["bvh"][1]["crossings"]}
+                "rtree_entry_ms": res["rtree"][2], "walk_ms": res["raster"][3],
+                "crossings_equal": all(res["raster"][1]["crossings"] == res[k][1]["crossings"]
+                                       for k in ("bvh", "rtree"))}
         print(json.dumps(line), flush=True)
         out.append(line)
     path = os.path.join(ROOT, "gpurun_out", "entry_compare.json")

@@ -108,10 +108,11 @@ enum { TET_TRAVERSE_EXACT = 0, TET_TRAVERSE_MT_F64 = 1, TET_TRAVERSE_MT_F32 = 2 
  * starts from):
  *   TET_ENTRY_RASTER : per (hull face, angle) exact rasterisation of the face's
  *                      detector footprint (default)
- *   TET_ENTRY_BVH    : per-ray search of a BVH over the hull faces (the
- *                      paper's tree-search approach, binary BVH for R*-tree)
- * Both take the same exact entering decision, so results are identical.     */
-enum { TET_ENTRY_RASTER = 0, TET_ENTRY_BVH = 1 };
+ *   TET_ENTRY_BVH    : per-ray search of a binary BVH over the hull faces
+ *   TET_ENTRY_RTREE  : per-ray depth-first search of the paper's R*-tree over
+ *                      the hull faces (fan-out 4..10)
+ * All take the same exact entering decision, so results are identical.      */
+enum { TET_ENTRY_RASTER = 0, TET_ENTRY_BVH = 1, TET_ENTRY_RTREE = 2 };
 typedef struct {
     int32_t traversal;         /* TET_TRAVERSE_*                                 */
     int32_t max_escalations;   /* MT modes: 12 (SPEC.md:314 reading)            */

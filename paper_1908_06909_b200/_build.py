@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtetproj.so")
-SOURCES = ["mesh_host.cpp", "kernels.cu", "api.cu"]
+SOURCES = ["mesh_host.cpp", "rtree_host.cpp", "kernels.cu", "api.cu"]
 HEADERS = ["internal.h"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC,-O2", "-shared", "-Xptxas", "-v"]

@@ -30,6 +30,7 @@ struct tet_mesh {
     void* d_perm = nullptr;
     void* d_bvh_nodes = nullptr;
     void* d_bvh_faces = nullptr;
+    void* d_rtree = nullptr;
     // private stream-ordered pool for per-call scratch: freed scratch stays
     // cached across this mesh's calls (no re-allocation inside timed calls)
     // and is returned to the device at tet_mesh_destroy; the device's default
@@ -265,7 +266,8 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
     if (!m) return fail(TET_E_ARG, "null mesh");
     const int mode = opt ? opt->traversal : TET_TRAVERSE_EXACT;
     const int entry_mode = opt ? opt->entry : TET_ENTRY_RASTER;
-    if (entry_mode != TET_ENTRY_RASTER && entry_mode != TET_ENTRY_BVH)
+    if (entry_mode != TET_ENTRY_RASTER && entry_mode != TET_ENTRY_BVH &&
+        entry_mode != TET_ENTRY_RTREE)
         return fail(TET_E_ARG, "unknown entry finder");
     if (mode < TET_TRAVERSE_EXACT || mode > TET_TRAVERSE_MT_F32)
         return fail(TET_E_ARG, "unknown traversal mode");
@@ -392,6 +394,8 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
                 KernelTimer kt(m, TET_K_ENTRY, sk);
                 if (entry_mode == TET_ENTRY_BVH)
                     CU(launch_entry_bvh(m->dev, c, ent, d_stats, sk));
+                else if (entry_mode == TET_ENTRY_RTREE)
+                    CU(launch_entry_rtree(m->dev, c, ent, d_stats, sk));
                 else
                     CU(launch_entry(m->dev, c, ent, entry_scratch[chunk_idx % nbuf], d_stats, sk));
             }
@@ -503,6 +507,7 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     if (e == cudaSuccess) e = up(&m->d_perm, H.perm.data(), H.perm.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_bvh_nodes, H.bvh_nodes.data(), H.bvh_nodes.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_bvh_faces, H.bvh_faces.data(), H.bvh_faces.size() * 4);
+    if (e == cudaSuccess) e = up(&m->d_rtree, H.rtree_nodes.data(), H.rtree_nodes.size() * 4);
     if (e != cudaSuccess) {
         tet_mesh_destroy(m);
         return cuda_fail(e, "tet_mesh_create upload");
@@ -515,6 +520,7 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     m->dev.perm = (const int*)m->d_perm;
     m->dev.bvh_nodes = (const int4*)m->d_bvh_nodes;
     m->dev.bvh_faces = (const int4*)m->d_bvh_faces;
+    m->dev.rtree = (const int*)m->d_rtree;
     m->dev.nv = H.nv;
     m->dev.nt = H.nt;
     m->dev.nb = H.nb;
@@ -545,6 +551,7 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     std::vector<int32_t>().swap(H.perm);
     std::vector<int32_t>().swap(H.bvh_nodes);
     std::vector<int32_t>().swap(H.bvh_faces);
+    std::vector<int32_t>().swap(H.rtree_nodes);
     *out = m;
     return TET_OK;
 }
@@ -566,6 +573,7 @@ tet_status tet_mesh_destroy(tet_mesh_t m) {
     cudaFree(m->d_perm);
     cudaFree(m->d_bvh_nodes);
     cudaFree(m->d_bvh_faces);
+    cudaFree(m->d_rtree);
     // returned to the device once the last stream-ordered free has run
     if (m->pool) cudaMemPoolDestroy(m->pool);
     delete m;

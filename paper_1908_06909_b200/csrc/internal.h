@@ -43,6 +43,7 @@ struct HostMesh {
     std::vector<int32_t> perm; // [T] internal -> caller tet index
     std::vector<int32_t> bvh_nodes;  // [N][8] float lo[3], hi[3] | left, right (leaf: -(first+1), count)
     std::vector<int32_t> bvh_faces;  // [B][4] vertex ids (outward order) | entry code tet<<2|k
+    std::vector<int32_t> rtree_nodes;  // [N][72] R*-tree over bvh_faces (rtree_host.cpp)
     double rmax = 0;           // max |X|_2 over vertices (grid units)
     double bs_c[3] = {0, 0, 0}, bs_r = 0;  // bounding sphere (grid units)
     bool reordered = false;
@@ -53,6 +54,9 @@ struct HostMesh {
 tet_status prepare_mesh(const double* verts, int64_t nv, const int32_t* tets,
                         const int32_t* nbrs, int64_t nt, const int32_t* bfaces,
                         int64_t nb, uint32_t flags, HostMesh& out, std::string& err);
+
+// The paper's R*-tree over the hull faces (fan-out 4..10), from bvh_faces.
+void build_hull_rtree(HostMesh& M);
 
 // Snap a geometry to the mesh grid and validate it.
 tet_status prepare_geometry(const HostMesh& m, const tet_geometry* g,
@@ -69,6 +73,7 @@ struct DevMesh {
     const int* perm = nullptr;   // [T]
     const int4* bvh_nodes = nullptr;  // [2N] hull-face BVH (TET_ENTRY_BVH)
     const int4* bvh_faces = nullptr;  // [B]
+    const int* rtree = nullptr;  // [N][72] R*-tree nodes (TET_ENTRY_RTREE)
     int64_t nv = 0, nt = 0, nb = 0;
     double g = 0, rmax = 0;
     double C[3] = {0, 0, 0};     // grid origin (world units)
@@ -115,6 +120,8 @@ cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry, voi
                          unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_entry_bvh(const DevMesh& m, const LaunchChunk& c, int* entry,
                              unsigned long long* stats, cudaStream_t s);
+cudaError_t launch_entry_rtree(const DevMesh& m, const LaunchChunk& c, int* entry,
+                               unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_forward(const DevMesh& m, const LaunchChunk& c, const int* entry,
                            const float* mu_int, float* proj, unsigned long long* stats,
                            cudaStream_t s);

@@ -814,6 +814,86 @@ __global__ void __launch_bounds__(128) entry_bvh_kernel(const int4* __restrict__
     if (lane == 0 && s) atomicAdd(stats + ST_EXACT, (unsigned long long)s);
 }
 
+// The paper's initialisation (TET_ENTRY_RTREE): "an
+// R*-tree is precomputed for the boundary elements ... To search the tree, a
+// depth-first algorithm is implemented ... When a leaf node is reached in the
+// search, all tetrahedra within that node are checked for intersection".
+// One thread per ray; nodes of <= 10 children (rtree_host.cpp); child boxes
+// tested like the BVH's (float, rounded outward, fp64 slab test with a
+// margin, so no face the ray meets is pruned); faces tested exactly.  The
+// paper keeps the leaf candidate with the minimum intersection parameter;
+// with exact signs exactly one hull face is entering, so the search stops at
+// it (reading R9).
+__device__ __forceinline__ bool ray_box(const double o[3], const double inv[3], const double d[3],
+                                        const float* lo, const float* hi) {
+    double tmin = -INFINITY, tmax = INFINITY;
+    for (int i = 0; i < 3; ++i) {
+        const double m = 2.0 + 1e-9 * (fabs((double)lo[i]) + fabs(o[i]));
+        const double l = (double)lo[i] - m, h = (double)hi[i] + m;
+        if (d[i] == 0.0) {
+            if (o[i] < l || o[i] > h) return false;
+        } else {
+            const double t1 = (l - o[i]) * inv[i], t2 = (h - o[i]) * inv[i];
+            tmin = fmax(tmin, fmin(t1, t2));
+            tmax = fmin(tmax, fmax(t1, t2));
+        }
+    }
+    return !(tmin > tmax + 1e-9 * (fabs(tmin) + fabs(tmax)));
+}
+
+__global__ void __launch_bounds__(128) entry_rtree_kernel(const int* __restrict__ nodes,
+                                                          const int4* __restrict__ faces,
+                                                          const int4* __restrict__ vtx,
+                                                          const AngleGeom* __restrict__ ang,
+                                                          int beam, int nv, int nu,
+                                                          int* __restrict__ entry,
+                                                          unsigned long long* __restrict__ stats) {
+    const int tiles_u = (nu + 15) >> 4;
+    const int bx = blockIdx.x % tiles_u, by = blockIdx.x / tiles_u;
+    const int a = blockIdx.y;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int u = bx * 16 + (w & 1) * 8 + (lane & 7);
+    const int v = by * 8 + (w >> 1) * 4 + (lane >> 3);
+    unsigned exact = 0;
+    if (u < nu && v < nv) {
+        const RayPts r = ray_points(ang[a], beam, u, v);
+        const double o[3] = {(double)r.ox, (double)r.oy, (double)r.oz};
+        const double d[3] = {(double)(r.px - r.ox), (double)(r.py - r.oy), (double)(r.pz - r.oz)};
+        double inv[3];
+        for (int i = 0; i < 3; ++i) inv[i] = 1.0 / d[i];   // +-inf for d = 0
+        int stack[96];
+        int sp = 0, found = -1;
+        stack[sp++] = 0;                                   // root
+        while (sp > 0 && found < 0) {
+            const int* nd = nodes + 72 * stack[--sp];
+            const int cnt = __ldg(nd), leaf = __ldg(nd + 1);
+            const float* lo = reinterpret_cast<const float*>(nd + 12);
+            const float* hi = reinterpret_cast<const float*>(nd + 42);
+            float blo[3], bhi[3];
+            if (leaf) {
+                for (int c = 0; c < cnt && found < 0; ++c) {
+                    for (int i = 0; i < 3; ++i) { blo[i] = __ldg(lo + 3 * c + i); bhi[i] = __ldg(hi + 3 * c + i); }
+                    if (!ray_box(o, inv, d, blo, bhi)) continue;
+                    const int4 fc = __ldg(faces + __ldg(nd + 2 + c));
+                    const int4 A = __ldg(vtx + fc.x), B = __ldg(vtx + fc.y), C = __ldg(vtx + fc.z);
+                    if (side_direct(A, B, r, exact) == -1 && side_direct(B, C, r, exact) == -1 &&
+                        side_direct(C, A, r, exact) == -1)
+                        found = fc.w;
+                }
+            } else {
+                // depth first: children pushed in reverse so child 0 is searched first
+                for (int c = cnt - 1; c >= 0; --c) {
+                    for (int i = 0; i < 3; ++i) { blo[i] = __ldg(lo + 3 * c + i); bhi[i] = __ldg(hi + 3 * c + i); }
+                    if (ray_box(o, inv, d, blo, bhi) && sp < 96) stack[sp++] = __ldg(nd + 2 + c);
+                }
+            }
+        }
+        if (found >= 0) entry[((size_t)a * nv + v) * nu + u] = found;
+    }
+    const unsigned s = __reduce_add_sync(0xffffffffu, exact);
+    if (lane == 0 && s) atomicAdd(stats + ST_EXACT, (unsigned long long)s);
+}
+
 // ------------------------------------------------------------ walker ----
 // float -> double at the point of use (volatile: nvcc would hoist a plain
 // conversion of the loop-invariant weight out of the loop and keep -- at 64
@@ -1514,6 +1594,14 @@ cudaError_t launch_entry_bvh(const DevMesh& m, const LaunchChunk& c, int* entry,
     const dim3 grid((unsigned)(((c.nu + 15) / 16) * ((c.nv + 7) / 8)), (unsigned)c.n_angles);
     entry_bvh_kernel<<<grid, 128, 0, s>>>(m.bvh_nodes, m.bvh_faces, m.vtx, c.ang, c.beam, c.nv,
                                           c.nu, entry, stats);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_entry_rtree(const DevMesh& m, const LaunchChunk& c, int* entry,
+                               unsigned long long* stats, cudaStream_t s) {
+    const dim3 grid((unsigned)(((c.nu + 15) / 16) * ((c.nv + 7) / 8)), (unsigned)c.n_angles);
+    entry_rtree_kernel<<<grid, 128, 0, s>>>(m.rtree, m.bvh_faces, m.vtx, c.ang, c.beam, c.nv,
+                                            c.nu, entry, stats);
     return cudaGetLastError();
 }
 

@@ -451,6 +451,7 @@ tet_status prepare_mesh(const double* verts, int64_t nv, const int32_t* tets,
         M.hull[2 * h + 1] = hull[h].second;
     }
     build_hull_bvh(M, P, T, hull, vnew);
+    build_hull_rtree(M);
     return TET_OK;
 }
 

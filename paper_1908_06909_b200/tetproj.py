@@ -53,7 +53,7 @@ class tet_stats(C.Structure):
 TET_TRAVERSE_EXACT, TET_TRAVERSE_MT_F64, TET_TRAVERSE_MT_F32 = 0, 1, 2
 
 
-TET_ENTRY_RASTER, TET_ENTRY_BVH = 0, 1
+TET_ENTRY_RASTER, TET_ENTRY_BVH, TET_ENTRY_RTREE = 0, 1, 2
 
 
 class tet_options(C.Structure):

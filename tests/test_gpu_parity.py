@@ -110,10 +110,13 @@ def test_many_angles_uniform_frame_chunks(beam):
     assert r["stats"]["rays_hit"] > geom.n_rays // 4
 
 
+@pytest.mark.parametrize("finder", ["bvh", "rtree"])
 @pytest.mark.parametrize("case", ["c1", "lattice", "c2"])
-def test_bvh_entry_finder_identical(case):
-    """NEXT-3: the per-ray BVH entry finder takes the same exact decisions as
-    the footprint rasteriser: identical projections and crossing counts."""
+def test_bvh_entry_finder_identical(case, finder):
+    """NEXT-3: the per-ray tree entry finders -- a binary BVH and the paper's
+    R*-tree (fan-out 4..10) -- take the same exact
+    decisions as the footprint rasteriser: identical projections and crossing
+    counts, and parity with the oracle."""
     import torch
 
     from paper_1908_06909_b200 import tetproj as T
@@ -130,12 +133,13 @@ def test_bvh_entry_finder_identical(case):
     tm = T.TetMesh.from_mesh(mesh)
     mu_d = torch.from_numpy(mu).cuda()
     a, sa = tm.project(geom, mu_d, stats=True)
-    b, sb = tm.project(geom, mu_d, stats=True, opts=T.options(entry=T.TET_ENTRY_BVH))
+    mode = T.TET_ENTRY_BVH if finder == "bvh" else T.TET_ENTRY_RTREE
+    b, sb = tm.project(geom, mu_d, stats=True, opts=T.options(entry=mode))
     assert torch.equal(a, b)
     assert sa["crossings"] == sb["crossings"] and sa["rays_hit"] == sb["rays_hit"]
-    # and the BVH-entry path against the oracle (forward, backward, adjoint)
+    # and the tree-entry path against the oracle (forward, backward, adjoint)
     y = np.random.default_rng(2).uniform(0.5, 1.5, geom.n_rays).astype(np.float32)
-    U.check_parity(mesh, geom, mu, y, opts=T.options(entry=T.TET_ENTRY_BVH))
+    U.check_parity(mesh, geom, mu, y, opts=T.options(entry=mode))
 
 
 def test_debug_build_bounds_checks():
