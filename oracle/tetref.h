@@ -71,6 +71,8 @@ typedef struct {
     int32_t max_escalations;   /* 12 (SPEC.md:314 reading)                    */
     double eps0;               /* 1e-9 ("eps <- 10^-9")        */
     double eps_growth;         /* 10   ("eps <- eps * 10")     */
+    int32_t no_swap_check;     /* 1: skip Alg. 2's swap check (pins what it does) */
+    int32_t _pad;
 } tetref_mt_options;
 
 typedef struct {

@@ -75,7 +75,7 @@ class Stats(C.Structure):
 
 class MtOptions(C.Structure):
     _fields_ = [("single", C.c_int32), ("max_escalations", C.c_int32), ("eps0", C.c_double),
-                ("eps_growth", C.c_double)]
+                ("eps_growth", C.c_double), ("no_swap_check", C.c_int32), ("_pad", C.c_int32)]
 
 
 class MtStats(C.Structure):
@@ -231,8 +231,9 @@ def side(o, p, a, b) -> int:
 
 
 # ---- NEXT-1: the paper's own traversal (Alg. 1 + Alg. 2), oracle/tetref_mt.inc ----
-def mt_options(single=False, eps0=1e-9, eps_growth=10.0, max_escalations=12):
-    return MtOptions(1 if single else 0, max_escalations, eps0, eps_growth)
+def mt_options(single=False, eps0=1e-9, eps_growth=10.0, max_escalations=12, swap_check=True):
+    return MtOptions(1 if single else 0, max_escalations, eps0, eps_growth,
+                     0 if swap_check else 1, 0)
 
 
 def mt_project(mesh: OracleMesh, geom, mu, single=False, ray_ids=None, nthreads: int = 0,

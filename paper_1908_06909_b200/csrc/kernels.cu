@@ -297,6 +297,23 @@ __device__ __forceinline__ int icomp(const int4 v, int k) {
     return selp(v.x, selp(v.y, v.z, k == 1), k == 0);
 }
 
+// Per-ray streams (entry map, y, proj: 377 MB each per c3 step, touched once)
+// go through L2 with the evict-first policy (ld/st .cs) so they do not
+// displace the mesh's face tags (TRACE_STREAM_HINTS, A/B knob).
+#ifndef TRACE_STREAM_HINTS
+#define TRACE_STREAM_HINTS 1
+#endif
+template <class V>
+__device__ __forceinline__ V ld_stream(const V* p) {
+    if (TRACE_STREAM_HINTS) return __ldcs(p);
+    return *p;
+}
+template <class V>
+__device__ __forceinline__ void st_stream(V* p, V v) {
+    if (TRACE_STREAM_HINTS) __stcs(p, v);
+    else *p = v;
+}
+
 // reciprocal: MUFU approximation (~2^-23) + one fp64 Newton step (~2^-46);
 // TRACE_RCP_NEWTON = 0 keeps the bare approximation (A/B knob)
 #ifndef TRACE_RCP_NEWTON
@@ -992,7 +1009,7 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
 #if TRACE_BWD_WY32
         // f32 weight: one register (at 64 registers the f64 weight spilled and
         // its local reload stalled every RED); relative error 2^-24
-        const float wy = BACK ? (float)((double)y[rid] * ray_scale<UNI>(F, U, g)) : 0.f;
+        const float wy = BACK ? (float)((double)ld_stream(y + rid) * ray_scale<UNI>(F, U, g)) : 0.f;
 #else
         const double wy = BACK ? (double)y[rid] * ray_scale<UNI>(F, U, g) : 0.0;
 #endif
@@ -1153,7 +1170,7 @@ __device__ __forceinline__ RayPts ft_scaled(RayPts r) {
 }
 
 template <bool BACK, int AX, int UNI, int BX, int BY, bool BAND>
-__device__ __forceinline__ void walk_ray_ft(const UniFrame& U, const int4* __restrict__ tag,
+__device__ __forceinline__ void walk_ray_ft(const UniFrame& Ug, const int4* __restrict__ tag,
                                             const int4* __restrict__ tnode,
                                             const int4* __restrict__ vtx,
                                             const AngleGeom* __restrict__ ang, int beam, int a,
@@ -1164,13 +1181,14 @@ __device__ __forceinline__ void walk_ray_ft(const UniFrame& U, const int4* __res
                                             double* __restrict__ acc, double& sum,
                                             unsigned& n_cross, unsigned& n_exact,
                                             unsigned& n_lost, unsigned& n_stuck) {
+    const UniFrame& U = Ug;
     const RayPts r = ft_scaled(ray_points(ang[a], beam, u, v));
     const double gs = g * (1.0 / (1 << kFtShift));
     Frame F;
     if constexpr (UNI == 0) make_frame_ax<AX>(r, rmax * (1 << kFtShift), gs, F);
     else make_frame_uni<AX, UNI>(r, U, F);
 #if TRACE_BWD_WY32
-    const float wy = BACK ? (float)((double)y[rid] * ray_scale<UNI>(F, U, gs)) : 0.f;
+    const float wy = BACK ? (float)((double)ld_stream(y + rid) * ray_scale<UNI>(F, U, gs)) : 0.f;
 #else
     const double wy = BACK ? (double)y[rid] * ray_scale<UNI>(F, U, gs) : 0.0;
 #endif
@@ -1289,7 +1307,7 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
     const int v = by * BY * th + (w / BX) * th + (lane >> tw_log);
     const bool valid = u < nu && v < nv;
     const size_t rid = ((size_t)a * nv + v) * nu + u;
-    const int e = valid ? entry[rid] : -1;
+    const int e = valid ? ld_stream(entry + rid) : -1;
 
     unsigned n_cross = 0, n_exact = 0, n_lost = 0, n_stuck = 0;
     double sum = 0.0;
@@ -1355,7 +1373,7 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
         }
 #undef WALK
     }
-    if (!BACK && valid) proj[rid] = (float)sum;
+    if (!BACK && valid) st_stream(proj + rid, (float)sum);
     add_stat(stats, ST_HIT, e >= 0 ? 1u : 0u);
     add_stat(stats, ST_CROSS, n_cross);
     add_stat(stats, ST_EXACT, n_exact);

@@ -174,3 +174,25 @@ def test_fig_singledouble_on_slivers():
     np.testing.assert_allclose(q64, p, rtol=1e-9, atol=1e-12)
     failed32 = s32["lost"] + s32["stuck"]
     assert failed32 > 0.1 * st["rays_hit"], s32
+
+
+def test_swap_check_prevents_backtracking():
+    """"An extra check thus needs to be performed when
+    zero-length intersections are found, to ensure there is no backtracking
+    by choosing the wrong face for the propagation of the ray, which can
+    happen when a node exist with several tetrahedra" (fig:bad).  On lattice
+    rays through the vertices of Kuhn meshes -- the fig:bad configuration --
+    Alg. 2 with the swap check leaves fewer rays stuck and gives more rays
+    the exact integral (the exact SoS walker's value) than without it."""
+    for n in (2, 3, 4):
+        m = M.kuhn_lattice(n)
+        om = O.OracleMesh.from_mesh(m)
+        geom = G.lattice_parallel((1 / n,) * 3, (0, 0, 0), 2 * n + 3, 2 * n + 3, G.LATTICE_DIRS)
+        mu = np.ones(m.n_tets)
+        p, _ = O.project(om, geom, mu)
+        q1, s1 = O.mt_project(om, geom, mu, swap_check=True)
+        q0, s0 = O.mt_project(om, geom, mu, swap_check=False)
+        exact1 = int((np.abs(q1 - p) <= 1e-9 * np.maximum(p, 1)).sum())
+        exact0 = int((np.abs(q0 - p) <= 1e-9 * np.maximum(p, 1)).sum())
+        assert s1["stuck"] < s0["stuck"], (n, s1, s0)
+        assert exact1 > exact0, (n, exact1, exact0)
