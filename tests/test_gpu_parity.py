@@ -196,14 +196,15 @@ def test_host_pointers_and_accumulate():
 
 
 def test_host_pointers_pipelined_chunks():
-    """Host buffers with more than one 2^23-ray chunk: y / proj move chunk by
+    """Host buffers over several pipelined chunks (18.4 M rays: 2^22-ray
+    chunks by the eighth-of-the-call rule): y / proj move chunk by
     chunk on a copy stream overlapped with tracing; results equal the
     device-pointer call (projections bit-exact, backprojection to f64-sum
     rounding)."""
     import torch
 
     from paper_1908_06909_b200 import tetproj as T
-    w = CF.workload("c2", n_angles=70, n_u=512, n_v=512)    # 18.4 M rays: 3 chunks
+    w = CF.workload("c2", n_angles=70, n_u=512, n_v=512)    # 18.4 M rays: 5 chunks
     tm = T.TetMesh.from_mesh(w.mesh)
     p_dev = tm.project(w.geom, torch.from_numpy(w.mu).cuda())
     x_dev = tm.backproject(w.geom, torch.from_numpy(w.y).cuda())
