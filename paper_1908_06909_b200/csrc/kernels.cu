@@ -68,8 +68,14 @@ typedef __int128 i128;
 #ifndef TRACE_BAND_ORDER
 #define TRACE_BAND_ORDER 1
 #endif
+#ifndef TRACE_BAND_BYTES_PER_TET
+#define TRACE_BAND_BYTES_PER_TET 32
+#endif
+// angles per band group of the backward walk on L2-exceeding meshes: 2 for
+// round 1's record walk, 4 for the FT16 walk (c5 backward 558 -> 548 ms;
+// 1: 591, 8: 552, 16: 558), profiles/README.md
 #ifndef TRACE_BWD_BAND_GROUP
-#define TRACE_BWD_BAND_GROUP 2
+#define TRACE_BWD_BAND_GROUP 4
 #endif
 #ifndef TRACE_EXACT_ONECALL
 #define TRACE_EXACT_ONECALL 1
@@ -1791,7 +1797,7 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     // angles through the same slab at once make its f64 REDs collide (full
     // band order: c3 backward 34.8 -> 52.9 ms).  L2-resident meshes keep
     // angle order (c3 forward 27.1 -> 27.3 ms with bands).
-    const bool big = TRACE_BAND_ORDER && (size_t)m.nt * 32 > l2_bytes() / 2;
+    const bool big = TRACE_BAND_ORDER && (size_t)m.nt * TRACE_BAND_BYTES_PER_TET > l2_bytes() / 2;
     const int group = big ? (BACK ? TRACE_BWD_BAND_GROUP : 1 << 20) : 0;
     const int tile_code = twl | group << 4;
     static thread_local UniFrames U;   // 10 KB: copied into the launch parameters
