@@ -1810,6 +1810,7 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
                    : (big ? trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, true, false>
                           : trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, false, false>);
     const int4* rec_or_tag = ft ? m.tag16 : m.rec;
+
     if (m.l2_window_bytes == 0) {
         kern<<<trace_grid_w(c, twl, S::BX, S::BY), 32 * S::BX * S::BY, 0, s>>>(TRACE_ARGS, tile_code,
                                                                                (int)m.nv, U);
