@@ -559,7 +559,8 @@ def main():
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
-            "config": config_dict(args, w, full_geom, geom, ws),
+            "config": dict(config_dict(args, w, full_geom, geom, ws),
+                           walk=T.tet_mesh_features(h)["walk"]),
             "fwd": {"crossings_per_s": cf_all / (statistics.median(ms_f) / 1e3),
                     "mrays_per_s": rays_all / (statistics.median(ms_f) / 1e3) / 1e6,
                     "ms": statistics.median(ms_f), "crossings": int(cf_all)},

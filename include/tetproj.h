@@ -180,6 +180,16 @@ tet_status tet_backproject_ex(tet_mesh_t m, const tet_geometry* g, const float* 
  * window bytes, reordered (0/1).                                              */
 tet_status tet_mesh_info(tet_mesh_t m, int64_t info[8]);
 
+/* Which walk and entry structures the mesh carries:
+ *   feat[0] = walk of exact traversals: 1 = FT16 (16-B face tags with apex
+ *             coordinates; exact-heavy scans still take the record walk),
+ *             0 = 32-B record walk (mesh beyond the FT16 encoding, or
+ *             TETPROJ_WALKER=rec at create)
+ *   feat[1] = bytes of FT16 tags on the device (0 without)
+ *   feat[2] = R*-tree nodes over the hull faces (TET_ENTRY_RTREE)
+ *   feat[3] = binary BVH nodes over the hull faces (TET_ENTRY_BVH)          */
+tet_status tet_mesh_features(tet_mesh_t m, int64_t feat[4]);
+
 /* Kernel timing for benchmarks / profiling.  When enabled, every call records
  * CUDA events around each of its kernel launches on the call's stream (no
  * synchronisation is added).  tet_kernel_times() -- only after that stream

@@ -37,6 +37,7 @@ struct tet_mesh {
     // pool -- shared with the rest of the process -- is never touched
     cudaMemPool_t pool = nullptr;
     int64_t bytes = 0;
+    int64_t tag16_bytes = 0, rtree_nodes = 0, bvh_nodes = 0;
     // kernel timing (tet_set_kernel_timing)
     struct TimerRec { int kind; cudaEvent_t a, b; };
     std::mutex tmu;
@@ -508,6 +509,9 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
     const char* wk = std::getenv("TETPROJ_WALKER");
     const bool ft16 = H.ft16 && !(wk && std::string(wk) == "rec");
     if (e == cudaSuccess && ft16) e = up(&m->d_tag16, H.tag16.data(), H.tag16.size() * 4);
+    m->tag16_bytes = ft16 ? (int64_t)H.tag16.size() * 4 : 0;
+    m->rtree_nodes = (int64_t)H.rtree_nodes.size() / 72;
+    m->bvh_nodes = (int64_t)H.bvh_nodes.size() / 8;
     if (e == cudaSuccess) e = up(&m->d_tnode, H.tnode.data(), H.tnode.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_vtx, H.vtx.data(), H.vtx.size() * 4);
     if (e == cudaSuccess) e = up(&m->d_hull, H.hull.data(), H.hull.size() * 4);
@@ -663,6 +667,15 @@ tet_status tet_kernel_times(tet_mesh_t m, double ms[4], int64_t launches[4]) {
         m->ms[k] = 0;
         m->launches[k] = 0;
     }
+    return TET_OK;
+}
+
+tet_status tet_mesh_features(tet_mesh_t m, int64_t feat[4]) {
+    if (!m || !feat) return fail(TET_E_ARG, "null argument");
+    feat[0] = m->dev.tag16 ? 1 : 0;
+    feat[1] = m->tag16_bytes;
+    feat[2] = m->rtree_nodes;
+    feat[3] = m->bvh_nodes;
     return TET_OK;
 }
 

@@ -69,8 +69,8 @@ def options(traversal: int = TET_TRAVERSE_EXACT, eps0: float = 1e-9, eps_growth:
 
 
 EXPORTS = ["tet_mesh_create", "tet_mesh_destroy", "tet_project", "tet_backproject",
-           "tet_backproject_f64", "tet_mesh_info", "tet_last_error", "tet_set_kernel_timing",
-           "tet_kernel_times", "tet_project_ex", "tet_backproject_ex"]
+           "tet_backproject_f64", "tet_mesh_info", "tet_mesh_features", "tet_last_error",
+           "tet_set_kernel_timing", "tet_kernel_times", "tet_project_ex", "tet_backproject_ex"]
 KERNEL_CLASSES = ["entry", "forward", "backward", "permute"]
 
 _lib = None
@@ -101,6 +101,7 @@ def lib(build: bool = False) -> C.CDLL:
     L.tet_backproject_f64.argtypes = [P, C.POINTER(tet_geometry), P, P, P,
                                       C.POINTER(tet_stats)]
     L.tet_mesh_info.argtypes = [P, C.POINTER(C.c_int64)]
+    L.tet_mesh_features.argtypes = [P, C.POINTER(C.c_int64)]
     L.tet_project_ex.argtypes = [P, C.POINTER(tet_geometry), P, P, C.POINTER(tet_options), P,
                                  C.POINTER(tet_stats)]
     L.tet_backproject_ex.argtypes = [P, C.POINTER(tet_geometry), P, P, C.c_int,
@@ -109,7 +110,7 @@ def lib(build: bool = False) -> C.CDLL:
     L.tet_kernel_times.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     L.tet_last_error.restype = C.c_char_p
     for f in ("tet_mesh_create", "tet_mesh_destroy", "tet_project", "tet_backproject",
-              "tet_backproject_f64", "tet_mesh_info", "tet_set_kernel_timing",
+              "tet_backproject_f64", "tet_mesh_info", "tet_mesh_features", "tet_set_kernel_timing",
               "tet_kernel_times", "tet_project_ex", "tet_backproject_ex"):
         getattr(L, f).restype = C.c_int
     _lib = L
@@ -205,6 +206,13 @@ def tet_mesh_info(m: MeshHandle) -> dict:
     keys = ["n_verts", "n_tets", "n_bfaces", "device", "grid_exponent", "device_bytes",
             "l2_window_bytes", "reordered"]
     return dict(zip(keys, [int(x) for x in info]))
+
+
+def tet_mesh_features(m: MeshHandle) -> dict:
+    feat = (C.c_int64 * 4)()
+    _check(lib().tet_mesh_features(m.ptr, feat))
+    return {"walk": "ft16" if feat[0] else "rec", "tag16_bytes": int(feat[1]),
+            "rtree_nodes": int(feat[2]), "bvh_nodes": int(feat[3])}
 
 
 def tet_set_kernel_timing(m: MeshHandle, enable: bool = True):

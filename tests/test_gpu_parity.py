@@ -472,3 +472,30 @@ def test_exact_heavy_walk_shape_same_results():
     _, xr, _, _ = U.run_oracle(w.mesh, w.geom, w.mu, w.y)
     be = U.back_errors(x0.cpu().numpy().astype(np.float64), xr)
     assert be.max() <= U.BACK_TOL, be.max()
+
+
+def test_mesh_features_walk_selection():
+    """The benchmark configs run the FT16 walk (16-B tags with apex
+    coordinates) and carry both tree entry structures; TETPROJ_WALKER=rec
+    (read at create) selects the record walk, with identical results."""
+    import os
+
+    import torch
+
+    from paper_1908_06909_b200 import tetproj as T
+    w = CF.workload("c2", n_angles=2, n_u=48, n_v=40)
+    tm = T.TetMesh.from_mesh(w.mesh)
+    f = T.tet_mesh_features(tm.handle)
+    assert f["walk"] == "ft16" and f["tag16_bytes"] == 64 * w.mesh.n_tets
+    assert f["rtree_nodes"] > 0 and f["bvh_nodes"] > 0
+    os.environ["TETPROJ_WALKER"] = "rec"
+    try:
+        tr = T.TetMesh.from_mesh(w.mesh)
+    finally:
+        del os.environ["TETPROJ_WALKER"]
+    assert T.tet_mesh_features(tr.handle)["walk"] == "rec"
+    mu = torch.from_numpy(w.mu).cuda()
+    a, sa = tm.project(w.geom, mu, stats=True)
+    b, sb = tr.project(w.geom, mu, stats=True)
+    assert sa["crossings"] == sb["crossings"]
+    np.testing.assert_allclose(a.cpu().numpy(), b.cpu().numpy(), rtol=1e-6, atol=1e-7)
