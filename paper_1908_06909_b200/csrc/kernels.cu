@@ -320,6 +320,38 @@ __device__ __forceinline__ void st_stream(V* p, V v) {
     else *p = v;
 }
 
+// Backprojection RED with an L2 evict-last policy on the accumulator lines
+// (TRACE_RED_EVICT_LAST, A/B knob): on meshes whose tags exceed the L2 the
+// accumulator competes with the tag stream.
+#ifndef TRACE_RED_EVICT_LAST
+#define TRACE_RED_EVICT_LAST 1
+#endif
+#ifndef TRACE_TAG_EVICT_LAST
+#define TRACE_TAG_EVICT_LAST 0
+#endif
+// FT16 tag load, optionally with an L2 evict-last policy (A/B knob)
+__device__ __forceinline__ int4 ld_tag(const int4* p) {
+#if TRACE_TAG_EVICT_LAST
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    int4 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+    return r;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ void red_acc(double* p, double v) {
+#if TRACE_RED_EVICT_LAST
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(pol) : "memory");
+#else
+    atomicAdd(p, v);
+#endif
+}
+
 // reciprocal: MUFU approximation (~2^-23) + one fp64 Newton step (~2^-46);
 // TRACE_RCP_NEWTON = 0 keeps the bare approximation (A/B knob)
 #ifndef TRACE_RCP_NEWTON
@@ -1247,7 +1279,7 @@ __device__ __forceinline__ void walk_ray_ft(const UniFrame& Ug, const int4* __re
         const int idj = selp(id0, selp(id1, id2, j == 1), j == 0);
         const int L = rank4(id0, id1, id2, iap, idj);
         // the exit face's tag: issued now, consumed after this step's chord
-        const int4 tg = __ldg(tag + 4 * (size_t)t + (j == 3 ? 0 : L));
+        const int4 tg = ld_tag(tag + 4 * (size_t)t + (j == 3 ? 0 : L));
         const int tcur = t;
         if (j == 0) { x0 = x3; y0 = y3; z0 = z3; id0 = iap; }
         if (j == 1) { x1 = x3; y1 = y3; z1 = z3; id1 = iap; }
@@ -1255,7 +1287,7 @@ __device__ __forceinline__ void walk_ray_ft(const UniFrame& Ug, const int4* __re
         const double zout = face_depth(x0, y0, z0, x1, y1, z1, x2, y2, z2, zin, n_exact);
         const double dz = zout - zin;
         if (BACK) {
-            if (dz > 0.0) atomicAdd(acc + tcur, dz * f2d_here(wy));
+            if (dz > 0.0) red_acc(acc + tcur, dz * f2d_here(wy));
         } else {
             sum = fma(dz, (double)mut, sum);
         }
