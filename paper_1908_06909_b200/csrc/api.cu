@@ -363,18 +363,43 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         // and <= kUniMaxAngles angles (one walker launch per chunk)
         const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(g->n_angles, kUniMaxAngles),
                                                                       max_chunk_rays / per_angle));
+        // Chunk schedule (angle counts).  With host buffers the first chunk's
+        // copy-in (backprojection) and the last chunk's copy-out (projection)
+        // cannot overlap any tracing, so those ends are tapered: c/4, c/4, c/2
+        // at the head and c/2, c/4, c/4 at the tail (TETPROJ_PIPE_TAPER=0: all c).
+        static const int taper_env = [] {
+            const char* e = getenv("TETPROJ_PIPE_TAPER");
+            return e ? atoi(e) : 1;
+        }();
+        std::vector<int> sizes;
+        {
+            int rem = g->n_angles;
+            const bool taper = taper_env && g->n_angles > 2 * chunk;
+            std::vector<int> head, tail;
+            if (taper && pipe_in) head = {std::max(1, chunk / 4), std::max(1, chunk / 4), std::max(1, chunk / 2)};
+            if (taper && pipe_out) tail = {std::max(1, chunk / 2), std::max(1, chunk / 4), std::max(1, chunk / 4)};
+            int tail_total = 0;
+            for (int t : tail) tail_total += t;
+            for (int h : head)
+                if (rem > tail_total) { const int t = std::min(h, rem - tail_total); sizes.push_back(t); rem -= t; }
+            while (rem > tail_total) { const int t = std::min(chunk, rem - tail_total); sizes.push_back(t); rem -= t; }
+            for (int t : tail)
+                if (rem > 0) { const int u = std::min(t, rem); sizes.push_back(u); rem -= u; }
+        }
         if (pipe_in) {   // all y chunks are queued at once; chunk k's trace waits for its copy
             CU(cs.after(s));
-            for (int a0 = 0; a0 < g->n_angles; a0 += chunk) {
+            int a0 = 0;
+            for (int na : sizes) {
                 const size_t off = (size_t)a0 * per_angle;
-                const size_t n = (size_t)std::min(chunk, g->n_angles - a0) * per_angle;
+                const size_t n = (size_t)na * per_angle;
                 CU(cudaMemcpyAsync((float*)d_in + off, (const float*)in + off, n * sizeof(float),
                                    cudaMemcpyHostToDevice, cs.s));
                 CU(cs.mark());
+                a0 += na;
             }
         }
         size_t chunk_idx = 0;
-        const int n_chunks = (g->n_angles + chunk - 1) / chunk;
+        const int n_chunks = (int)sizes.size();
         const int nbuf = n_chunks > 1 ? 2 : 1;
         int* entry[2] = {nullptr, nullptr};
         void* entry_scratch[2] = {nullptr, nullptr};
@@ -391,8 +416,8 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         const int heavy = heavy_env >= 0 ? (heavy_env != 0) : m->exact_heavy.load();
         AuxStream ws(m, s, n_chunks > 1);
         if (ws.err != cudaSuccess) return cuda_fail(ws.err, "walk stream");
-        for (int a0 = 0; a0 < g->n_angles; a0 += chunk) {
-            const int na = std::min(chunk, g->n_angles - a0);
+        int a0 = 0;
+        for (const int na : sizes) {
             cudaStream_t sk = ws.get(chunk_idx);
             int* ent = entry[chunk_idx % nbuf];
             LaunchChunk c{d_ang + a0, ang.data() + a0, d_aux + a0, g->beam, na, g->n_v, g->n_u};
@@ -429,6 +454,7 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
                                    (size_t)na * per_angle * sizeof(float), cudaMemcpyDeviceToHost,
                                    cs.s));
             }
+            a0 += na;
         }
         CU(ws.join());
         if (pipe_out) CU(cs.join(s));
