@@ -50,7 +50,7 @@ def _case(seed):
     return mesh, geom, mu, y
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", range(48))
 def test_random_scans_match_oracle(seed):
     from paper_1908_06909_b200 import tetproj as T
     mesh, geom, mu, y = _case(seed)
@@ -62,3 +62,23 @@ def test_random_scans_match_oracle(seed):
         U.check_parity(mesh, geom, mu, y, opts=T.options(entry=entry))
     finally:
         os.environ.pop("TETPROJ_WALKER", None)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_scans_paper_mode_match_mt_oracle(seed):
+    """The paper's Alg. 1/2 walk (fp64 for even seeds, fp32 for odd) on the
+    same random scans: bit-identical projections and equal crossing, lost,
+    stuck and escalation counts against the MT oracle."""
+    import torch
+
+    from oracle import tetref as O
+    from paper_1908_06909_b200 import tetproj as T
+    mesh, geom, mu, y = _case(seed)
+    single = bool(seed % 2)
+    tm = T.TetMesh.from_mesh(mesh)
+    mode = T.TET_TRAVERSE_MT_F32 if single else T.TET_TRAVERSE_MT_F64
+    p, st = tm.project(geom, torch.from_numpy(mu).cuda(), stats=True, opts=T.options(mode))
+    q, ost = O.mt_project(O.OracleMesh.from_mesh(mesh), geom, mu.astype(np.float64), single=single)
+    for k in ("rays_hit", "crossings", "lost", "stuck", "escalations"):
+        assert st[k] == ost[k], (k, st, ost)
+    np.testing.assert_array_equal(p.cpu().numpy().ravel(), q.astype(np.float32).ravel())
