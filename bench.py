@@ -541,8 +541,9 @@ def main():
         clk = clocks.summary()
         rl = roofline(args.config, dom, cross_unit / per_step_launches,
                       tdom / max(launches, 1), clk.get("sm_mhz"))
-        # each timed entry region launches two kernels (setup + raster)
-        n_launch_step = (nf + nb + 2 * ne + np_) / args.steps
+        # each timed entry region launches three kernels (setup, small-item
+        # raster, warp raster)
+        n_launch_step = (nf + nb + 3 * ne + np_) / args.steps
         line = {
             "metric": METRIC,
             "value": (cf_all + cb_all) / (med / 1e3),

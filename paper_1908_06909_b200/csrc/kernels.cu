@@ -62,6 +62,13 @@ typedef __int128 i128;
 #ifndef TRACE_PAR_UNI
 #define TRACE_PAR_UNI 1
 #endif
+// footprints of at most this many pixels go to entry_small_kernel (thread
+// per item); 0 sends every item to the warp raster.  c4a (36,300 hull faces
+// of ~1 px at lattice pitch): entry 0.88 -> 0.34 ms per step at 32 px; c2
+// (~50-px boxes) 0.58 -> 0.59, c3 unchanged; 128 / 256 px cost c2 0.75 / 1.02
+#ifndef ENTRY_SMALL_PX
+#define ENTRY_SMALL_PX 32u
+#endif
 #ifndef ENTRY_GUIDE
 #define ENTRY_GUIDE 4u
 #endif
@@ -563,7 +570,8 @@ struct EntryItem {
 __global__ void __launch_bounds__(128) entry_setup_kernel(
     const int4* __restrict__ tnode, const int4* __restrict__ vtx, const int2* __restrict__ hull,
     int nb, const AngleGeom* __restrict__ ang, const AngleAux* __restrict__ aux, int beam,
-    int n_angles, int nv, int nu, EntryItem* __restrict__ items, unsigned* __restrict__ n_items) {
+    int n_angles, int nv, int nu, EntryItem* __restrict__ items, unsigned* __restrict__ n_items,
+    unsigned cap, unsigned small_px) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= nb * n_angles) return;
     const int h = idx % nb, a = idx / nb;
@@ -661,13 +669,72 @@ __global__ void __launch_bounds__(128) entry_setup_kernel(
     it.npx = (u1 - u0 + 1) * (v1 - v0 + 1);
     it.code = (hk.x << 2) | k;
     it.pad[0] = it.pad[1] = it.pad[2] = 0;
-    // compacted item list (order irrelevant: each ray has one entering face)
-    const unsigned mask = __activemask();
+    // compacted item lists (order irrelevant: each ray has one entering
+    // face): footprints of <= small_px pixels from the end of the array
+    // (counter n_items[2]; one thread per item, entry_small_kernel), larger
+    // ones from the front (counter n_items[0]; a warp per item)
+    const unsigned act = __activemask();
+    const bool small = (unsigned)it.npx <= small_px;
+    const unsigned mask = __ballot_sync(act, small) ^ (small ? 0u : act);   // lanes of my kind
     const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
     unsigned slot = 0;
-    if (lane == leader) slot = atomicAdd(n_items, (unsigned)__popc(mask));
+    if (lane == leader) slot = atomicAdd(n_items + (small ? 2 : 0), (unsigned)__popc(mask));
     slot = __shfl_sync(mask, slot, leader) + __popc(mask & ((1u << lane) - 1));
-    items[slot] = it;
+    items[small ? cap - 1 - slot : slot] = it;
+}
+
+__device__ __noinline__ bool exact_entering(const int4* __restrict__ vtx,
+                                            const AngleGeom* __restrict__ ang, int beam, int a,
+                                            int u, int v, int ia, int ib, int ic,
+                                            unsigned& exact);
+
+// Small footprints (beside the warp raster): one thread per (face, angle)
+// item tests every pixel of its <= small_px-pixel box with the item's exact
+// affine sides (certified by the bound, else int128 + SoS), the same test
+// as the warp raster's dense pass; a warp per pixel-sized item (c4a's
+// lattice hull) left most lanes idle.
+__global__ void __launch_bounds__(128) entry_small_kernel(
+    const int4* __restrict__ vtx, const AngleGeom* __restrict__ ang, int beam, int nv, int nu,
+    const EntryItem* __restrict__ items, unsigned cap, const unsigned* __restrict__ n_small_p,
+    int* __restrict__ entry, unsigned long long* __restrict__ stats) {
+    const unsigned idx = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned conflicts = 0, exact = 0;
+    if (idx < n_small_p[0]) {
+        const EntryItem* it = items + (cap - 1 - idx);
+        const double c0 = it->c[0], al0 = it->al[0], be0 = it->be[0], b0 = it->bnd[0];
+        const double c1 = it->c[1], al1 = it->al[1], be1 = it->be[1], b1 = it->bnd[1];
+        const double c2 = it->c[2], al2 = it->al[2], be2 = it->be[2], b2 = it->bnd[2];
+        const int bw = it->bw, u0 = it->u0, v0 = it->v0, a = it->a, code = it->code;
+        const int nrows = it->npx / bw;
+        for (int r = 0; r < nrows; ++r) {
+            const int v = v0 + r;
+            const double fv = (double)v;
+            const double r0 = fma(fv, be0, c0), r1 = fma(fv, be1, c1), r2 = fma(fv, be2, c2);
+            for (int k = 0; k < bw; ++k) {
+                const int u = u0 + k;
+                const double fu = (double)u;
+                const double sab = fma(fu, al0, r0);
+                if (sab > b0) continue;
+                const double sbc = fma(fu, al1, r1);
+                if (sbc > b1) continue;
+                const double sca = fma(fu, al2, r2);
+                if (sca > b2) continue;
+                if (sab >= -b0 || sbc >= -b1 || sca >= -b2) {
+                    if (!exact_entering(vtx, ang, beam, a, u, v, it->ia, it->ib, it->ic, exact))
+                        continue;
+                }
+                DBG_CHECK(u < nu && v < nv);
+                const int old = atomicExch(entry + ((size_t)a * nv + v) * nu + u, code);
+                conflicts += (old != -1);
+            }
+        }
+    }
+    const unsigned cs = __reduce_add_sync(0xffffffffu, conflicts);
+    const unsigned es = __reduce_add_sync(0xffffffffu, exact);
+    if ((threadIdx.x & 31) == 0) {
+        if (cs) atomicAdd(stats + ST_CONFLICT, (unsigned long long)cs);
+        if (es) atomicAdd(stats + ST_EXACT, (unsigned long long)es);
+    }
 }
 
 // Rare path of the entry test: all three signs decided by side_direct (fp64
@@ -1663,14 +1730,17 @@ cudaError_t launch_entry_rtree(const DevMesh& m, const LaunchChunk& c, int* entr
 
 cudaError_t launch_entry(const DevMesh& m, const LaunchChunk& c, int* entry, void* scratch,
                          unsigned long long* stats, cudaStream_t s) {
-    unsigned* n_items = (unsigned*)scratch;
+    unsigned* n_items = (unsigned*)scratch;   // [0] large items, [1] queue, [2] small items
     EntryItem* items = (EntryItem*)((char*)scratch + 256);
     const long long n = (long long)m.nb * c.n_angles;
-    cudaError_t e = cudaMemsetAsync(n_items, 0, 2 * sizeof(unsigned), s);   // count, queue
+    cudaError_t e = cudaMemsetAsync(n_items, 0, 3 * sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
     entry_setup_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
         m.tnode, m.vtx, m.hull, (int)m.nb, c.ang, c.aux, c.beam, c.n_angles, c.nv, c.nu, items,
-        n_items);
+        n_items, (unsigned)n, ENTRY_SMALL_PX);
+    if (ENTRY_SMALL_PX > 0)
+        entry_small_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
+            m.vtx, c.ang, c.beam, c.nv, c.nu, items, (unsigned)n, n_items + 2, entry, stats);
     static const unsigned grid = [] {
         int dev = 0, sms = 148, per = 8;
         cudaGetDevice(&dev);
