@@ -499,3 +499,38 @@ def test_mesh_features_walk_selection():
     b, sb = tr.project(w.geom, mu, stats=True)
     assert sa["crossings"] == sb["crossings"]
     np.testing.assert_allclose(a.cpu().numpy(), b.cpu().numpy(), rtol=1e-6, atol=1e-7)
+
+
+def test_strict_flag_reports_failed_rays():
+    """TET_F_STRICT: a call whose statistics show lost or stuck rays fails with
+    TET_E_RAYS (header contract).  The exact walk never produces one; the
+    paper's fp32 traversal on slivers does (fig:singledouble)."""
+    import torch
+
+    from paper_1908_06909_b200 import tetproj as T
+    mesh, geom, mu, y = _mt_case("slivers")
+    tm = T.TetMesh.from_mesh(mesh, flags=T.TET_F_FIX_ORIENTATION | T.TET_F_STRICT)
+    mu_d = torch.from_numpy(mu).cuda()
+    p, st = tm.project(geom, mu_d, stats=True)                 # exact: passes
+    assert st["lost"] == st["stuck"] == 0
+    with pytest.raises(T.TetProjError) as e:
+        tm.project(geom, mu_d, opts=T.options(T.TET_TRAVERSE_MT_F32))
+    assert e.value.status == T.TET_E_RAYS
+
+
+def test_backproject_accumulate_device():
+    """x += A^T y on device pointers: two accumulating calls give twice the
+    backprojection, and match the oracle."""
+    import torch
+
+    from paper_1908_06909_b200 import tetproj as T
+    w = CF.workload("c2", n_angles=2, n_u=40, n_v=32)
+    tm = T.TetMesh.from_mesh(w.mesh)
+    yd = torch.from_numpy(w.y).cuda()
+    x = torch.zeros(w.mesh.n_tets, device="cuda")
+    T.tet_backproject(tm.handle, w.geom, yd, x, accumulate=True)
+    T.tet_backproject(tm.handle, w.geom, yd, x, accumulate=True)
+    torch.cuda.synchronize()
+    _, xr, _, _ = U.run_oracle(w.mesh, w.geom, w.mu, w.y)
+    be = U.back_errors(x.cpu().numpy().astype(np.float64) / 2, xr)
+    assert be.max() <= U.BACK_TOL, be.max()
