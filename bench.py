@@ -374,7 +374,11 @@ def nccl_report(rank, log_path):
     """NCCL version and, from the INIT log of this rank, whether NVLS
     (NVSwitch in-switch reduction) was set up."""
     import torch
-    out = {"version": ".".join(str(v) for v in torch.cuda.nccl.version())}
+    try:
+        v = torch.cuda.nccl.version()
+        out = {"version": ".".join(str(x) for x in v) if isinstance(v, (tuple, list)) else str(v)}
+    except Exception as e:   # reporting only: never fail the benchmark over it
+        out = {"version": f"unknown ({type(e).__name__})"}
     try:
         txt = open(log_path).read()
         out["log"] = os.path.relpath(log_path, ROOT)
