@@ -6,8 +6,11 @@ arXiv:1908.06909 on B200, per BASELINE.json's metric.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
                   [--scaling weak|strong] [--angles A] [--impl reference]
 
-One JSON line on rank 0.  A step = tet_project(mu) + tet_backproject(y) over
-the rank's angles, the backprojection all-reduced over NCCL for N > 1.
+One JSON line on rank 0.  A step = tet_plan_create (geometry + the entry map
+of every ray, Alg. 2 "Read initial intersection element") +
+tet_plan_project(mu) + tet_plan_backproject(y) + tet_plan_destroy over the
+rank's angles, the backprojection all-reduced over NCCL for N > 1 (--no-plan:
+tet_project + tet_backproject, each running the entry finder itself).
 --scaling weak (default): every rank owns A angles (default: the config's)
 of an N*A-angle circular scan.  --scaling strong: the config's scan (or
 --angles total angles) is sharded over the N ranks (north_star c5: 720
@@ -51,6 +54,8 @@ def parse(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-plan", action="store_true",
+                    help="entry finder inside each call instead of once per step")
     ap.add_argument("--angles", type=int, default=None,
                     help="weak: angles per rank; strong: total angles (default: the config's)")
     return ap.parse_args(argv)
@@ -447,16 +452,33 @@ def main():
     assert st_f["lost"] == st_f["stuck"] == st_f["entry_conflicts"] == 0, st_f
     assert st_b["lost"] == st_b["stuck"] == 0, st_b
 
-    def backward():
+    use_plan = not args.no_plan
+
+    def forward(mu_in, proj_out, **kw):
+        """The step's first half; returns the plan (None with --no-plan)."""
+        if not use_plan:
+            T.tet_project(h, geom, mu_in, proj_out, **kw)
+            return None
+        pl = T.tet_plan_create(h, geom, stream=stream.cuda_stream)   # entry map, once per step
+        T.tet_plan_project(pl, mu_in, proj_out, **kw)
+        return pl
+
+    def back_local(pl, y_in, x_out, **kw):
+        if pl is None:
+            T.tet_backproject(h, geom, y_in, x_out, **kw)
+        else:
+            T.tet_plan_backproject(pl, y_in, x_out, **kw)
+            T.tet_plan_destroy(pl)          # stream-ordered free
+
+    def backward(pl):
         if ws > 1:   # local A_r^T y_r, then all_reduce(SUM) over NCCL
             dist_backproject(tm, full_geom, y,
-                             backproject=lambda g, yl: (T.tet_backproject(h, g, yl, x), x)[1])
+                             backproject=lambda g, yl: (back_local(pl, yl, x), x)[1])
         else:
-            T.tet_backproject(h, geom, y, x)
+            back_local(pl, y, x)
 
     def step():
-        T.tet_project(h, geom, mu, proj)
-        backward()
+        backward(forward(mu, proj))
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -474,9 +496,9 @@ def main():
         for i in range(args.steps):
             flush.zero_()                    # L2 flush between timed steps (not timed)
             ev[i][0].record(stream)
-            T.tet_project(h, geom, mu, proj)
+            pl = forward(mu, proj)
             ev[i][1].record(stream)
-            backward()
+            backward(pl)
             ev[i][2].record(stream)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
@@ -516,8 +538,8 @@ def main():
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        T.tet_project(h, geom, mu_h.numpy(), proj_h.numpy(), stream=stream.cuda_stream)
-        T.tet_backproject(h, geom, y_h.numpy(), x_h.numpy(), stream=stream.cuda_stream)
+        pl = forward(mu_h.numpy(), proj_h.numpy(), stream=stream.cuda_stream)
+        back_local(pl, y_h.numpy(), x_h.numpy(), stream=stream.cuda_stream)
         if ws > 1:
             xd = x_h.to(dev, non_blocking=True)
             dist.all_reduce(xd)
@@ -546,7 +568,7 @@ def main():
         rl = roofline(args.config, dom, cross_unit / per_step_launches,
                       tdom / max(launches, 1), clk.get("sm_mhz"))
         # each timed entry region launches three kernels (setup, small-item
-        # raster, warp raster)
+        # raster, warp raster): once per step with a plan, once per call without
         n_launch_step = (nf + nb + 3 * ne + np_) / args.steps
         line = {
             "metric": METRIC,
@@ -565,7 +587,9 @@ def main():
             "dtype": "f64",
             "data": "synthetic",
             "config": dict(config_dict(args, w, full_geom, geom, ws),
-                           walk=T.tet_mesh_features(h)["walk"]),
+                           walk=T.tet_mesh_features(h)["walk"],
+                           entry=("once per step (tet_plan_create), shared by fwd and back"
+                                  if use_plan else "per call (tet_project, tet_backproject)")),
             "fwd": {"crossings_per_s": cf_all / (statistics.median(ms_f) / 1e3),
                     "mrays_per_s": rays_all / (statistics.median(ms_f) / 1e3) / 1e6,
                     "ms": statistics.median(ms_f), "crossings": int(cf_all)},

@@ -175,6 +175,42 @@ tet_status tet_backproject_ex(tet_mesh_t m, const tet_geometry* g, const float* 
                               int accumulate, const tet_options* opt, void* cuda_stream,
                               tet_stats* st);
 
+/* Plans: a scan bound to a mesh.  PAPER.md Alg. 2 (lines 120-144) starts each
+ * ray by "Read initial intersection element": the entry tet of every ray is
+ * an input of the walk, and for a fixed scan it is the same for every
+ * projection and backprojection.  tet_plan_create validates and snaps the
+ * geometry once and runs the entry finder (opt->entry) for all rays into a
+ * device entry map (4 B per ray, from the mesh's memory pool); the plan's
+ * project / backproject calls walk from that map and skip the entry stage.
+ * Results are identical to tet_project / tet_backproject with the same
+ * geometry and options (the same kernels on the same entry map; backprojection
+ * sums are rounded from double, so only the atomics' order differs).
+ *   g, opt  host; copied (the caller's arrays are not retained); opt NULL =
+ *           exact traversal, raster entry finder
+ *   stream  creation is stream-ordered on cuda_stream: the plan may be used on
+ *           that stream at once, on another one after synchronising with it
+ *   *out    owned by the caller until tet_plan_destroy; the mesh must outlive
+ *           it.  Plans are immutable: concurrent calls on different streams
+ *           are safe.
+ * Errors: TET_E_ARG (null / unknown option), TET_E_GEOMETRY (as tet_project),
+ * TET_E_NOMEM / TET_E_CUDA (device); on error *out = NULL.                   */
+typedef struct tet_plan* tet_plan_t;
+tet_status tet_plan_create(tet_mesh_t m, const tet_geometry* g, const tet_options* opt,
+                           void* cuda_stream, tet_plan_t* out);
+/* Releases the plan's device memory stream-ordered on cuda_stream (which must
+ * be ordered after every use of the plan, as for cudaFreeAsync).  NULL is a
+ * no-op. */
+tet_status tet_plan_destroy(tet_plan_t p, void* cuda_stream);
+/* tet_project / tet_backproject / tet_backproject_f64 on the plan's scan and
+ * options; same array contracts, stats include the entry finder's counters
+ * (exact_fallbacks, entry_conflicts) from tet_plan_create. */
+tet_status tet_plan_project(tet_plan_t p, const float* mu, float* proj, void* cuda_stream,
+                            tet_stats* st);
+tet_status tet_plan_backproject(tet_plan_t p, const float* proj, float* x, int accumulate,
+                                void* cuda_stream, tet_stats* st);
+tet_status tet_plan_backproject_f64(tet_plan_t p, const float* proj, double* acc,
+                                    void* cuda_stream, tet_stats* st);
+
 /* Introspection (for tests / bench).  info[0..7] = n_verts, n_tets, n_bfaces,
  * device, grid exponent e (g = 2^e), bytes of device mesh data, L2 persisting
  * window bytes, reordered (0/1).                                              */

@@ -68,6 +68,22 @@ struct tet_mesh {
     }
 };
 
+// A scan bound to a mesh (tet_plan_create): the snapped geometry tables and
+// the entry map of every ray, computed once and shared by the plan's calls.
+struct tet_plan {
+    tet_mesh* m = nullptr;
+    tet_geometry g{};
+    std::vector<double> vecs;
+    tet_options opt{};
+    bool has_opt = false;
+    std::vector<tetproj::AngleGeom> ang;
+    std::vector<tetproj::AngleAux> aux;
+    tetproj::AngleGeom* d_ang = nullptr;
+    tetproj::AngleAux* d_aux = nullptr;
+    int* d_entry = nullptr;                    // [n_angles][n_v][n_u], -1 = miss
+    unsigned long long* d_stats = nullptr;     // the entry finder's counters
+};
+
 namespace {
 
 thread_local std::string g_err;
@@ -145,7 +161,8 @@ cudaError_t make_pool(int dev, cudaMemPool_t* pool) {
     return cudaMemPoolSetAttribute(*pool, cudaMemPoolAttrReleaseThreshold, &thr);
 }
 
-enum class Op { Forward, Backward, BackwardF64 };
+// Entry: only the entry finder, into a plan's entry map (tet_plan_create)
+enum class Op { Forward, Backward, BackwardF64, Entry };
 
 cudaEvent_t take_event(tet_mesh* m) {
     cudaEvent_t e = nullptr;
@@ -262,9 +279,14 @@ struct CopyStream {
 };
 
 // Shared driver: geometry prep, chunking over angles, entry finder, walker.
+// With a plan, the geometry tables and the entry map are the plan's (op
+// Entry computes that map; the other ops skip the entry finder).
 tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, int accumulate,
-               Op op, void* stream, tet_stats* st, const tet_options* opt = nullptr) {
+               Op op, void* stream, tet_stats* st, const tet_options* opt = nullptr,
+               tet_plan* plan = nullptr) {
     if (!m) return fail(TET_E_ARG, "null mesh");
+    const bool entry_only = op == Op::Entry;
+    const bool use_plan = plan && !entry_only;
     const int mode = opt ? opt->traversal : TET_TRAVERSE_EXACT;
     const int entry_mode = opt ? opt->entry : TET_ENTRY_RASTER;
     if (entry_mode != TET_ENTRY_RASTER && entry_mode != TET_ENTRY_BVH &&
@@ -280,25 +302,30 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         mto.eps_growth = opt->eps_growth;
         mto.max_escalations = opt->max_escalations;
     }
-    if (!g || !in || !out) return fail(TET_E_ARG, "null argument");
-    std::vector<AngleGeom> ang;
-    std::vector<AngleAux> aux;
-    std::string err;
-    tet_status rs = prepare_geometry(m->host, g, ang, aux, err);
-    if (rs != TET_OK) return fail(rs, err);
+    if (!g || (!entry_only && (!in || !out))) return fail(TET_E_ARG, "null argument");
+    if (entry_only && !plan) return fail(TET_E_ARG, "entry map without a plan");
+    std::vector<AngleGeom> ang_own;
+    std::vector<AngleAux> aux_own;
+    if (!plan) {
+        std::string err;
+        tet_status rs = prepare_geometry(m->host, g, ang_own, aux_own, err);
+        if (rs != TET_OK) return fail(rs, err);
+    }
+    const std::vector<AngleGeom>& ang = plan ? plan->ang : ang_own;
+    const std::vector<AngleAux>& aux = plan ? plan->aux : aux_own;
     DeviceGuard guard(m->device);
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t nrays = (int64_t)g->n_angles * g->n_v * g->n_u;
     const int64_t nt = m->dev.nt;
     bool wd_in = false, wd_out = false;
-    const bool dev_in = is_device_ptr(in, m->device, wd_in);
-    const bool dev_out = is_device_ptr(out, m->device, wd_out);
+    const bool dev_in = entry_only || is_device_ptr(in, m->device, wd_in);
+    const bool dev_out = entry_only || is_device_ptr(out, m->device, wd_out);
     if (wd_in || wd_out) return fail(TET_E_ARG, "device pointer on another device than the mesh");
     if (op == Op::BackwardF64 && !dev_out) return fail(TET_E_ARG, "tet_backproject_f64 needs a device accumulator");
     const size_t in_bytes = (op == Op::Forward ? nt : nrays) * sizeof(float);
     const size_t out_elems = (op == Op::Forward ? nrays : nt);
     const bool strict = (m->flags & TET_F_STRICT) != 0;
-    const bool need_stats = st || strict;
+    const bool need_stats = !entry_only && (st || strict);
     unsigned long long hs[ST_COUNT] = {0};
     {
         Scratch sc(s, m->pool);  // released (stream-ordered) at the end of this scope
@@ -323,20 +350,35 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
             if (op == Op::Backward && accumulate)
                 CU(cudaMemcpyAsync(d_out, out, out_elems * sizeof(float), cudaMemcpyHostToDevice, s));
         }
-        // --- geometry tables
+        // --- geometry tables (a plan's are on the device already)
         AngleGeom* d_ang;
         AngleAux* d_aux;
         unsigned long long* d_stats;
-        CU(sc.alloc((void**)&d_ang, sizeof(AngleGeom) * ang.size()));
-        CU(sc.alloc((void**)&d_aux, sizeof(AngleAux) * aux.size()));
-        CU(sc.alloc((void**)&d_stats, sizeof(unsigned long long) * ST_COUNT));
-        CU(cudaMemcpyAsync(d_ang, ang.data(), sizeof(AngleGeom) * ang.size(), cudaMemcpyHostToDevice, s));
-        CU(cudaMemcpyAsync(d_aux, aux.data(), sizeof(AngleAux) * aux.size(), cudaMemcpyHostToDevice, s));
-        CU(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * ST_COUNT, s));
+        if (plan) {
+            d_ang = plan->d_ang;
+            d_aux = plan->d_aux;
+        } else {
+            CU(sc.alloc((void**)&d_ang, sizeof(AngleGeom) * ang.size()));
+            CU(sc.alloc((void**)&d_aux, sizeof(AngleAux) * aux.size()));
+            CU(cudaMemcpyAsync(d_ang, ang.data(), sizeof(AngleGeom) * ang.size(), cudaMemcpyHostToDevice, s));
+            CU(cudaMemcpyAsync(d_aux, aux.data(), sizeof(AngleAux) * aux.size(), cudaMemcpyHostToDevice, s));
+        }
+        if (entry_only) {
+            d_stats = plan->d_stats;
+            CU(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * ST_COUNT, s));
+        } else {
+            CU(sc.alloc((void**)&d_stats, sizeof(unsigned long long) * ST_COUNT));
+            if (use_plan)   // the counters start from the entry finder's (conflicts, exact)
+                CU(cudaMemcpyAsync(d_stats, plan->d_stats, sizeof(unsigned long long) * ST_COUNT,
+                                   cudaMemcpyDeviceToDevice, s));
+            else
+                CU(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * ST_COUNT, s));
+        }
         // --- per-op buffers
         float* mu_int = nullptr;
         double* acc = nullptr;
-        if (op == Op::Forward) {
+        if (entry_only) {
+        } else if (op == Op::Forward) {
             CU(sc.alloc((void**)&mu_int, nt * sizeof(float)));
             KernelTimer kt(m, TET_K_PERMUTE, s);
             CU(launch_gather_mu(m->dev, d_in, mu_int, s));
@@ -403,8 +445,8 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         const int nbuf = n_chunks > 1 ? 2 : 1;
         int* entry[2] = {nullptr, nullptr};
         void* entry_scratch[2] = {nullptr, nullptr};
-        for (int b = 0; b < nbuf; ++b) {
-            CU(sc.alloc((void**)&entry[b], sizeof(int) * per_angle * chunk));
+        for (int b = 0; b < nbuf && !use_plan; ++b) {
+            if (!entry_only) CU(sc.alloc((void**)&entry[b], sizeof(int) * per_angle * chunk));
             CU(sc.alloc(&entry_scratch[b], entry_scratch_bytes(m->dev, chunk)));
         }
         // chunk k runs on ws.get(k) with entry buffer k % 2 (the chunk k-2
@@ -419,11 +461,12 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         int a0 = 0;
         for (const int na : sizes) {
             cudaStream_t sk = ws.get(chunk_idx);
-            int* ent = entry[chunk_idx % nbuf];
+            const size_t off = (size_t)a0 * per_angle;
+            int* ent = plan ? plan->d_entry + off : entry[chunk_idx % nbuf];
             LaunchChunk c{d_ang + a0, ang.data() + a0, d_aux + a0, g->beam, na, g->n_v, g->n_u};
             c.exact_heavy = heavy;
-            CU(cudaMemsetAsync(ent, 0xff, sizeof(int) * per_angle * na, sk));
-            {
+            if (!use_plan) {
+                CU(cudaMemsetAsync(ent, 0xff, sizeof(int) * per_angle * na, sk));
                 KernelTimer kt(m, TET_K_ENTRY, sk);
                 if (entry_mode == TET_ENTRY_BVH)
                     CU(launch_entry_bvh(m->dev, c, ent, d_stats, sk));
@@ -432,7 +475,11 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
                 else
                     CU(launch_entry(m->dev, c, ent, entry_scratch[chunk_idx % nbuf], d_stats, sk));
             }
-            const size_t off = (size_t)a0 * per_angle;
+            if (entry_only) {
+                ++chunk_idx;
+                a0 += na;
+                continue;
+            }
             const bool fwd = op == Op::Forward;
             if (pipe_in) CU(cudaStreamWaitEvent(sk, cs.ev[chunk_idx], 0));
             ++chunk_idx;
@@ -641,6 +688,89 @@ tet_status tet_backproject(tet_mesh_t m, const tet_geometry* g, const float* pro
 tet_status tet_backproject_f64(tet_mesh_t m, const tet_geometry* g, const float* proj,
                                double* acc, void* cuda_stream, tet_stats* st) {
     return run(m, g, proj, acc, 1, Op::BackwardF64, cuda_stream, st);
+}
+
+tet_status tet_plan_create(tet_mesh_t m, const tet_geometry* g, const tet_options* opt,
+                           void* cuda_stream, tet_plan_t* out) {
+    if (!out) return fail(TET_E_ARG, "null argument");
+    *out = nullptr;
+    if (!m || !g || !g->vecs) return fail(TET_E_ARG, "null argument");
+    if (opt && opt->entry != TET_ENTRY_RASTER && opt->entry != TET_ENTRY_BVH &&
+        opt->entry != TET_ENTRY_RTREE)
+        return fail(TET_E_ARG, "unknown entry finder");
+    if (opt && (opt->traversal < TET_TRAVERSE_EXACT || opt->traversal > TET_TRAVERSE_MT_F32))
+        return fail(TET_E_ARG, "unknown traversal mode");
+    tet_plan* p = new tet_plan;
+    p->m = m;
+    p->g = *g;
+    if (g->n_angles > 0) p->vecs.assign(g->vecs, g->vecs + (size_t)g->n_angles * 12);
+    p->g.vecs = p->vecs.data();
+    if (opt) {
+        p->opt = *opt;
+        p->has_opt = true;
+    }
+    std::string err;
+    tet_status rs = prepare_geometry(m->host, g, p->ang, p->aux, err);
+    if (rs != TET_OK) {
+        delete p;
+        return fail(rs, err);
+    }
+    DeviceGuard guard(m->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const size_t nrays = (size_t)g->n_angles * g->n_v * g->n_u;
+    auto alloc = [&](void** q, size_t n) { return cudaMallocFromPoolAsync(q, n ? n : 16, m->pool, s); };
+    cudaError_t e = alloc((void**)&p->d_ang, sizeof(AngleGeom) * p->ang.size());
+    if (e == cudaSuccess) e = alloc((void**)&p->d_aux, sizeof(AngleAux) * p->aux.size());
+    if (e == cudaSuccess) e = alloc((void**)&p->d_entry, sizeof(int) * nrays);
+    if (e == cudaSuccess) e = alloc((void**)&p->d_stats, sizeof(unsigned long long) * ST_COUNT);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(p->d_ang, p->ang.data(), sizeof(AngleGeom) * p->ang.size(), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(p->d_aux, p->aux.data(), sizeof(AngleAux) * p->aux.size(), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) {
+        tet_plan_destroy(p, cuda_stream);
+        return cuda_fail(e, "tet_plan_create");
+    }
+    rs = run(m, &p->g, nullptr, nullptr, 0, Op::Entry, cuda_stream, nullptr,
+             p->has_opt ? &p->opt : nullptr, p);
+    if (rs != TET_OK) {
+        const std::string msg = g_err;
+        tet_plan_destroy(p, cuda_stream);
+        return fail(rs, msg);
+    }
+    *out = p;
+    return TET_OK;
+}
+
+tet_status tet_plan_destroy(tet_plan_t p, void* cuda_stream) {
+    if (!p) return TET_OK;
+    DeviceGuard guard(p->m->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    for (void* q : {(void*)p->d_ang, (void*)p->d_aux, (void*)p->d_entry, (void*)p->d_stats})
+        if (q) cudaFreeAsync(q, s);
+    delete p;
+    return TET_OK;
+}
+
+tet_status tet_plan_project(tet_plan_t p, const float* mu, float* proj, void* cuda_stream,
+                            tet_stats* st) {
+    if (!p) return fail(TET_E_ARG, "null plan");
+    return run(p->m, &p->g, mu, proj, 0, Op::Forward, cuda_stream, st,
+               p->has_opt ? &p->opt : nullptr, p);
+}
+
+tet_status tet_plan_backproject(tet_plan_t p, const float* proj, float* x, int accumulate,
+                                void* cuda_stream, tet_stats* st) {
+    if (!p) return fail(TET_E_ARG, "null plan");
+    return run(p->m, &p->g, proj, x, accumulate, Op::Backward, cuda_stream, st,
+               p->has_opt ? &p->opt : nullptr, p);
+}
+
+tet_status tet_plan_backproject_f64(tet_plan_t p, const float* proj, double* acc,
+                                    void* cuda_stream, tet_stats* st) {
+    if (!p) return fail(TET_E_ARG, "null plan");
+    return run(p->m, &p->g, proj, acc, 1, Op::BackwardF64, cuda_stream, st,
+               p->has_opt ? &p->opt : nullptr, p);
 }
 
 tet_status tet_set_kernel_timing(tet_mesh_t m, int enable) {

@@ -70,7 +70,9 @@ def options(traversal: int = TET_TRAVERSE_EXACT, eps0: float = 1e-9, eps_growth:
 
 EXPORTS = ["tet_mesh_create", "tet_mesh_destroy", "tet_project", "tet_backproject",
            "tet_backproject_f64", "tet_mesh_info", "tet_mesh_features", "tet_last_error",
-           "tet_set_kernel_timing", "tet_kernel_times", "tet_project_ex", "tet_backproject_ex"]
+           "tet_set_kernel_timing", "tet_kernel_times", "tet_project_ex", "tet_backproject_ex",
+           "tet_plan_create", "tet_plan_destroy", "tet_plan_project", "tet_plan_backproject",
+           "tet_plan_backproject_f64"]
 KERNEL_CLASSES = ["entry", "forward", "backward", "permute"]
 
 _lib = None
@@ -108,11 +110,16 @@ def lib(build: bool = False) -> C.CDLL:
                                      C.POINTER(tet_options), P, C.POINTER(tet_stats)]
     L.tet_set_kernel_timing.argtypes = [P, C.c_int]
     L.tet_kernel_times.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    L.tet_plan_create.argtypes = [P, C.POINTER(tet_geometry), C.POINTER(tet_options), P,
+                                  C.POINTER(C.c_void_p)]
+    L.tet_plan_destroy.argtypes = [P, P]
+    L.tet_plan_project.argtypes = [P, P, P, P, C.POINTER(tet_stats)]
+    L.tet_plan_backproject.argtypes = [P, P, P, C.c_int, P, C.POINTER(tet_stats)]
+    L.tet_plan_backproject_f64.argtypes = [P, P, P, P, C.POINTER(tet_stats)]
     L.tet_last_error.restype = C.c_char_p
-    for f in ("tet_mesh_create", "tet_mesh_destroy", "tet_project", "tet_backproject",
-              "tet_backproject_f64", "tet_mesh_info", "tet_mesh_features", "tet_set_kernel_timing",
-              "tet_kernel_times", "tet_project_ex", "tet_backproject_ex"):
-        getattr(L, f).restype = C.c_int
+    for f in EXPORTS:
+        if f != "tet_last_error":
+            getattr(L, f).restype = C.c_int
     _lib = L
     return L
 
@@ -271,6 +278,152 @@ def tet_backproject_f64(m: MeshHandle, geom, proj, acc, stream=None, stats: bool
     return st.as_dict() if stats else None
 
 
+@dataclass
+class PlanHandle:
+    ptr: C.c_void_p
+    mesh: MeshHandle          # the mesh must outlive the plan
+    n_rays: int
+    stream: int               # creation stream: the default stream of the destroy
+
+    def __del__(self):
+        if self.ptr is not None and _lib is not None and self.mesh.ptr is not None:
+            _lib.tet_plan_destroy(self.ptr, C.c_void_p(self.stream))
+            self.ptr = None
+
+
+def tet_plan_create(m: MeshHandle, geom, opts: tet_options | None = None,
+                    stream=None) -> PlanHandle:
+    """Bind a scan to the mesh: geometry snapped once, entry map of every ray
+    computed once (Alg. 2 "Read initial intersection element")."""
+    g, keep = _geom(geom)
+    h = C.c_void_p()
+    sv = _stream(stream)
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                sv = C.c_void_p(torch.cuda.current_stream(m.device).cuda_stream)
+        except ImportError:
+            pass
+    _check(lib().tet_plan_create(m.ptr, C.byref(g), C.byref(opts) if opts is not None else None,
+                                 sv, C.byref(h)))
+    return PlanHandle(h, m, geom.n_angles * geom.n_v * geom.n_u, int(sv.value or 0))
+
+
+def tet_plan_destroy(p: PlanHandle, stream=None):
+    if p.ptr is not None:
+        _check(lib().tet_plan_destroy(p.ptr, C.c_void_p(int(stream)) if stream is not None
+                                      else C.c_void_p(p.stream)))
+        p.ptr = None
+
+
+def tet_plan_project(p: PlanHandle, mu, proj, stream=None, stats: bool = False):
+    _, pmu = _ptr(mu, np.float32, p.mesh.n_tets)
+    _, pp = _ptr(proj, np.float32, p.n_rays)
+    st = tet_stats()
+    _check(lib().tet_plan_project(p.ptr, pmu, pp, _stream(stream, mu, proj),
+                                  C.byref(st) if stats else None))
+    return st.as_dict() if stats else None
+
+
+def tet_plan_backproject(p: PlanHandle, proj, x, accumulate: bool = False, stream=None,
+                         stats: bool = False):
+    _, pp = _ptr(proj, np.float32, p.n_rays)
+    _, px = _ptr(x, np.float32, p.mesh.n_tets)
+    st = tet_stats()
+    _check(lib().tet_plan_backproject(p.ptr, pp, px, 1 if accumulate else 0,
+                                      _stream(stream, proj, x), C.byref(st) if stats else None))
+    return st.as_dict() if stats else None
+
+
+def tet_plan_backproject_f64(p: PlanHandle, proj, acc, stream=None, stats: bool = False):
+    _, pp = _ptr(proj, np.float32, p.n_rays)
+    _, pa = _ptr(acc, np.float64, p.mesh.n_tets)
+    st = tet_stats()
+    _check(lib().tet_plan_backproject_f64(p.ptr, pp, pa, _stream(stream, proj, acc),
+                                          C.byref(st) if stats else None))
+    return st.as_dict() if stats else None
+
+
+class Plan:
+    """A scan bound to a TetMesh (tet_plan_create): project / backproject
+    without re-running the entry finder.  Use as a context manager or close()."""
+
+    def __init__(self, mesh: "TetMesh", geom, opts: tet_options | None = None, stream=None):
+        self.mesh = mesh
+        self.geom = geom
+        self.handle = tet_plan_create(mesh.handle, geom, opts, stream)
+
+    def close(self, stream=None):
+        tet_plan_destroy(self.handle, stream)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def project(self, mu, out=None, stats: bool = False):
+        import torch
+        if out is None:
+            g = self.geom
+            out = torch.empty((g.n_angles, g.n_v, g.n_u), dtype=torch.float32,
+                              device=mu.device if isinstance(mu, torch.Tensor) else "cpu")
+        st = tet_plan_project(self.handle, mu, out, stats=stats)
+        return (out, st) if stats else out
+
+    def backproject(self, proj, out=None, accumulate=False, stats: bool = False):
+        import torch
+        if out is None:
+            out = torch.zeros(self.mesh.n_tets, dtype=torch.float32,
+                              device=proj.device if isinstance(proj, torch.Tensor) else "cpu")
+        st = tet_plan_backproject(self.handle, proj, out, accumulate, stats=stats)
+        return (out, st) if stats else out
+
+    def backproject_f64(self, proj, out=None, stats: bool = False):
+        import torch
+        if out is None:
+            out = torch.zeros(self.mesh.n_tets, dtype=torch.float64,
+                              device=proj.device if isinstance(proj, torch.Tensor) else "cpu")
+        st = tet_plan_backproject_f64(self.handle, proj, out, stats=stats)
+        return (out, st) if stats else out
+
+
+class PlannedOperators:
+    """``project(geom, mu)`` / ``backproject(geom, y)`` callables for the
+    solvers (paper_1908_06909_b200.solvers) that bind each distinct scan --
+    e.g. each OS-SART subset -- to a plan on first use, so the entry finder
+    runs once per scan instead of once per call.  Plans live until close()."""
+
+    def __init__(self, mesh: "TetMesh", opts: tet_options | None = None):
+        self.mesh, self.opts, self.plans = mesh, opts, {}
+
+    def plan(self, geom) -> Plan:
+        vecs = np.ascontiguousarray(geom.vecs, dtype=np.float64)
+        key = (int(geom.beam), int(geom.n_v), int(geom.n_u), vecs.tobytes())
+        p = self.plans.get(key)
+        if p is None:
+            p = self.plans[key] = self.mesh.plan(geom, self.opts)
+        return p
+
+    def project(self, geom, mu):
+        return self.plan(geom).project(mu)
+
+    def backproject(self, geom, y):
+        return self.plan(geom).backproject(y)
+
+    def close(self):
+        for p in self.plans.values():
+            p.close()
+        self.plans.clear()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
 class TetMesh:
     """Convenience wrapper: a mesh resident on one GPU plus torch-facing ops."""
 
@@ -289,6 +442,10 @@ class TetMesh:
 
     def info(self) -> dict:
         return tet_mesh_info(self.handle)
+
+    def plan(self, geom, opts: tet_options | None = None, stream=None) -> Plan:
+        """Bind a scan: the entry finder runs once, here (tet_plan_create)."""
+        return Plan(self, geom, opts, stream)
 
     def project(self, geom, mu, out=None, stats: bool = False, opts=None):
         import torch

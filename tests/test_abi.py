@@ -42,6 +42,14 @@ def test_null_arguments_are_statuses():
     assert L.tet_project(None, None, None, None, None, None) == tetproj.TET_E_ARG
     assert L.tet_backproject(None, None, None, None, 0, None, None) == tetproj.TET_E_ARG
     assert L.tet_mesh_destroy(None) == tetproj.TET_OK
+    h = C.c_void_p(1)
+    assert L.tet_plan_create(None, None, None, None, C.byref(h)) == tetproj.TET_E_ARG
+    assert h.value is None                      # *out cleared on error
+    assert L.tet_plan_create(None, None, None, None, None) == tetproj.TET_E_ARG
+    assert L.tet_plan_project(None, None, None, None, None) == tetproj.TET_E_ARG
+    assert L.tet_plan_backproject(None, None, None, 0, None, None) == tetproj.TET_E_ARG
+    assert L.tet_plan_backproject_f64(None, None, None, None, None) == tetproj.TET_E_ARG
+    assert L.tet_plan_destroy(None, None) == tetproj.TET_OK
     assert isinstance(L.tet_last_error(), bytes)
 
 

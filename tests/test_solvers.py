@@ -124,25 +124,33 @@ def test_distributed_cgls_matches_single_process(tmp_path):
 
 
 @pytest.mark.gpu
-def test_gpu_os_sart_known_mesh():
+@pytest.mark.parametrize("ops", ["calls", "plans"])
+def test_gpu_os_sart_known_mesh(ops):
     """OS-SART on the CUDA operators, the paper's known-mesh setting
-    (fig:rec (a)): data simulated on the same mesh, 50 iterations, blocks of 20."""
+    (fig:rec (a)): data simulated on the same mesh, 50 iterations, blocks of 20
+    -- through the plain calls and through one plan per subset."""
     from paper_1908_06909_b200 import TetMesh
+    from paper_1908_06909_b200.tetproj import PlannedOperators
     from workloads import configs as CF
     w = CF.workload("c2", n_angles=40, n_u=64, n_v=64)
     tm = TetMesh.from_mesh(w.mesh)
     mu = torch.from_numpy(w.mu).cuda()
     b = tm.project(w.geom, mu)
     res = []
-    x = S.os_sart(lambda g, x: tm.project(g, x), lambda g, y: tm.backproject(g, y), w.geom, b,
-                  torch.zeros_like(mu), n_iter=50, block=20,
-                  callback=lambda it, x: res.append(float((tm.project(w.geom, x) - b).norm())))
+    with PlannedOperators(tm) as po:
+        P, B = ((lambda g, x: tm.project(g, x), lambda g, y: tm.backproject(g, y))
+                if ops == "calls" else (po.project, po.backproject))
+        x = S.os_sart(P, B, w.geom, b, torch.zeros_like(mu), n_iter=50, block=20,
+                      callback=lambda it, x: res.append(float((tm.project(w.geom, x) - b).norm())))
+        if ops == "plans":
+            assert len(po.plans) == 2          # 40 angles in blocks of 20: one plan per subset
     assert res[-1] < 0.05 * float(b.norm())
     assert res[-1] < res[0]
 
 
 @pytest.mark.gpu
-def test_gpu_solvers_match_oracle_operators():
+@pytest.mark.parametrize("ops", ["calls", "plans"])
+def test_gpu_solvers_match_oracle_operators(ops):
     """NEXT-2 parity: the same solver code on the CUDA operators and on the
     oracle operators, from the same data b, gives the same iterates -- every
     one of the first 5 CGLS and OS-SART iterates within 1e-4 (relative 2-norm)
@@ -153,6 +161,10 @@ def test_gpu_solvers_match_oracle_operators():
     tm = TetMesh.from_mesh(mesh)
     PG = lambda g, x: tm.project(g, x)          # noqa: E731
     BG = lambda g, y: tm.backproject(g, y)      # noqa: E731
+    if ops == "plans":
+        from paper_1908_06909_b200.tetproj import PlannedOperators
+        po = PlannedOperators(tm)
+        PG, BG = po.project, po.backproject
     b64 = P(geom, torch.from_numpy(mu))
     b32 = b64.float().cuda()
     z64 = torch.zeros(mesh.n_tets, dtype=torch.float64)
