@@ -390,9 +390,12 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
         // With host copies pipelined, the first chunk's copy-in and the last
         // chunk's copy-out are exposed while every chunk costs a fixed
         // overhead: about an eighth of the call's rays per chunk, within
-        // [2^22, 2^25] (c3, 94 M rays: 1.568e11 at 2^23, 1.573e11 at 2^24,
-        // 1.527e11 at 2^25; c5, 755 M rays: 1.610e11 at 2^23, 1.638e11 at 2^25
-        // crossings/s end to end; TETPROJ_PIPE_CHUNK_LOG forces a size)
+        // [2^21, 2^25] (c3, 94 M rays: 1.568e11 at 2^23, 1.573e11 at 2^24,
+        // 1.527e11 at 2^25; c5, 755 M rays: 1.610e11 at 2^23, 1.638e11 at 2^25;
+        // c2, 5.9 M rays: 1.364e11 at 2^22, 1.477e11 at 2^21, 1.493e11 at 2^20;
+        // c4a, 4.2 M rays with latency-bound walks: 8.99e9 at 2^22, 9.81e9 at
+        // 2^21, 6.95e9 at 2^20 crossings/s end to end; TETPROJ_PIPE_CHUNK_LOG
+        // forces a size)
         const int64_t per_angle = (int64_t)g->n_v * g->n_u;
         static const int pipe_log = [] {   // A/B knob for the host-buffer pipeline
             const char* e = getenv("TETPROJ_PIPE_CHUNK_LOG");
@@ -400,7 +403,7 @@ tet_status run(tet_mesh_t m, const tet_geometry* g, const float* in, void* out, 
             return v >= 16 && v <= 26 ? v : 0;
         }();
         const int64_t pipe_rays = pipe_log ? (1LL << pipe_log)
-                                           : std::max<int64_t>(1LL << 22, std::min<int64_t>(1LL << 25, nrays / 8));
+                                           : std::max<int64_t>(1LL << 21, std::min<int64_t>(1LL << 25, nrays / 8));
         const int64_t max_chunk_rays = (pipe_in || pipe_out) ? pipe_rays : (1LL << 26);
         // and <= kUniMaxAngles angles (one walker launch per chunk)
         const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(g->n_angles, kUniMaxAngles),
