@@ -198,8 +198,9 @@ typedef struct tet_plan* tet_plan_t;
 tet_status tet_plan_create(tet_mesh_t m, const tet_geometry* g, const tet_options* opt,
                            void* cuda_stream, tet_plan_t* out);
 /* Releases the plan's device memory stream-ordered on cuda_stream (which must
- * be ordered after every use of the plan, as for cudaFreeAsync).  NULL is a
- * no-op. */
+ * be ordered after every use of the plan, as for cudaFreeAsync) into the
+ * mesh's memory pool, where later calls and plans reuse it; the pool returns
+ * it to the device at tet_mesh_destroy.  NULL is a no-op. */
 tet_status tet_plan_destroy(tet_plan_t p, void* cuda_stream);
 /* tet_project / tet_backproject / tet_backproject_f64 on the plan's scan and
  * options; same array contracts, stats include the entry finder's counters
