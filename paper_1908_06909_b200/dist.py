@@ -63,16 +63,34 @@ def sharding_for(geom, group=None) -> AngleSharding:
     return AngleSharding(geom.n_angles, rank, world)
 
 
-def dist_project(mesh, geom, mu, group=None, project=None):
+def local_plan(mesh, geom, group=None, opts=None):
+    """A plan (tet_plan_create: geometry + entry map computed once) of this
+    rank's angles of the full scan ``geom``, for ``dist_project`` /
+    ``dist_backproject(plan=...)`` across iterations."""
+    return mesh.plan(sharding_for(geom, group).local_geometry(geom), opts)
+
+
+def _check_plan(plan, lg):
+    g = plan.geom
+    if (g.n_angles, g.n_v, g.n_u) != (lg.n_angles, lg.n_v, lg.n_u) or not np.array_equal(
+            np.asarray(g.vecs), np.asarray(lg.vecs)):
+        raise ValueError("plan is not of this rank's angles (use dist.local_plan)")
+
+
+def dist_project(mesh, geom, mu, group=None, project=None, plan=None):
     """Forward projection of this rank's angles (no communication).
-    Returns (local_proj, sharding)."""
+    Returns (local_proj, sharding).  ``plan``: this rank's ``local_plan``."""
     sh = sharding_for(geom, group)
+    lg = sh.local_geometry(geom)
+    if plan is not None:
+        _check_plan(plan, lg)
+        return plan.project(mu), sh
     fn = project if project is not None else mesh.project
-    return fn(sh.local_geometry(geom), mu), sh
+    return fn(lg, mu), sh
 
 
 def dist_backproject(mesh, geom, y_local, group=None, backproject=None, async_op=False,
-                     precision: str = "f32"):
+                     precision: str = "f32", plan=None):
     """x = A^T y over all ranks: local backprojection of this rank's angles,
     then all_reduce(SUM).  ``y_local`` holds this rank's rows
     (``AngleSharding.local_stack``).  Returns the reduced per-tet tensor
@@ -82,17 +100,21 @@ def dist_backproject(mesh, geom, y_local, group=None, backproject=None, async_op
     accumulation on the device, rounded once to float) is summed in float --
     W ranks add at most W * 2^-24 relative (R15).  "f64": each rank
     accumulates into a double tensor (tet_backproject_f64) and the double
-    partial sums are reduced; the result stays float64."""
+    partial sums are reduced; the result stays float64.  ``plan``: this
+    rank's ``local_plan`` (the entry map is not recomputed)."""
     import torch.distributed as dist
     sh = sharding_for(geom, group)
     lg = sh.local_geometry(geom)
-    if backproject is not None:
+    if precision not in ("f32", "f64"):
+        raise ValueError(f"precision must be 'f32' or 'f64', not {precision!r}")
+    if plan is not None:
+        _check_plan(plan, lg)
+        x = plan.backproject_f64(y_local) if precision == "f64" else plan.backproject(y_local)
+    elif backproject is not None:
         x = backproject(lg, y_local)
     elif precision == "f64":
         x = mesh.backproject_f64(lg, y_local)
-    elif precision == "f32":
-        x = mesh.backproject(lg, y_local)
     else:
-        raise ValueError(f"precision must be 'f32' or 'f64', not {precision!r}")
+        x = mesh.backproject(lg, y_local)
     work = dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
     return (x, work) if async_op else x

@@ -52,9 +52,14 @@ def _dist_worker(rank, world, port, out):
         x = D.dist_backproject(tm, w.geom, y_local)
         x64 = D.dist_backproject(tm, w.geom, y_local, precision="f64")
         p_local, _ = D.dist_project(tm, w.geom, torch.from_numpy(w.mu).cuda(dev))
-        torch.cuda.synchronize()
+        with D.local_plan(tm, w.geom) as pl:     # the same through this rank's plan
+            xp = D.dist_backproject(tm, w.geom, y_local, plan=pl)
+            xp64 = D.dist_backproject(tm, w.geom, y_local, precision="f64", plan=pl)
+            pp, _ = D.dist_project(tm, w.geom, torch.from_numpy(w.mu).cuda(dev), plan=pl)
+            torch.cuda.synchronize()
         res = {"x": x.cpu().numpy(), "x64": x64.cpu().numpy(),
-               "p": p_local.cpu().numpy(), "backend": dist.get_backend()}
+               "p": p_local.cpu().numpy(), "backend": dist.get_backend(),
+               "xp": xp.cpu().numpy(), "xp64": xp64.cpu().numpy(), "pp": pp.cpu().numpy()}
         np.savez(f"{out}.{rank}.npz", **res)
         dist.barrier()
     finally:
@@ -79,6 +84,10 @@ def test_two_rank_cuda_operators_match_oracle(tmp_path):
         idx = AngleSharding(w.geom.n_angles, rank, 2).local_angles()
         fe = U.fwd_errors(r["p"].astype(np.float64), pr[idx], w.mu, w.mesh)
         assert fe.max() <= U.FWD_TOL, fe.max()
+        # through the rank's plan: the same projection bits, the same sums
+        np.testing.assert_array_equal(r["pp"], r["p"])
+        np.testing.assert_allclose(r["xp"], r["x"], rtol=1e-6, atol=0)
+        np.testing.assert_allclose(r["xp64"], r["x64"], rtol=1e-12, atol=0)
 
 
 def _cgls_worker(rank, world, port, out):
