@@ -1,11 +1,6 @@
-# round-2 GPU check: GPU tests, smoke, default bench, reference arm, microbench + ncu of it
-set -x
+# full GPU check: every -m gpu test, smoke, the default bench line, the reference arm
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 2400 python -m pytest tests -m gpu -q -rf > gpurun_out/gpu_tests.log 2>&1; echo "GPU_TESTS_EXIT $?" >> gpurun_out/gpu_tests.log
-tail -5 gpurun_out/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > gpurun_out/smoke.txt 2>&1; tail -2 gpurun_out/smoke.txt
-timeout 900 python bench.py > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo "bench c3 $?"
-timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "bench ref $?"
-timeout 300 python experiments/microbench.py > gpurun_out/microbench.out 2>&1; echo "micro $?"
-timeout 600 ncu --metrics gpu__time_duration.sum,lts__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sectors_op_read.sum,lts__t_sector_hit_rate.pct,l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed,l1tex__t_sector_hit_rate.pct,dram__bytes_read.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum,l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum --clock-control none --csv -k regex:gather python experiments/microbench.py > gpurun_out/ncu_microbench.csv 2> gpurun_out/ncu_microbench.err; echo "ncu micro $?"
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/check_tests.log 2>&1; echo "tests $?"; tail -3 gpurun_out/check_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/check_smoke.log 2>&1; echo "smoke $?"; tail -1 gpurun_out/check_smoke.log
+timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/check_bench_c3.json 2> gpurun_out/check_bench_c3.err; echo "bench $?"
+tail -c 600 gpurun_out/check_bench_c3.json
