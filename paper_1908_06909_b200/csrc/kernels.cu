@@ -62,6 +62,9 @@ typedef __int128 i128;
 #ifndef TRACE_PAR_UNI
 #define TRACE_PAR_UNI 1
 #endif
+#ifndef TRACE_EMPTY_EXIT
+#define TRACE_EMPTY_EXIT 1
+#endif
 // footprints of at most this many pixels go to entry_small_kernel (thread
 // per item); 0 sends every item to the warp raster.  c4a (36,300 hull faces
 // of ~1 px at lattice pitch): entry 0.88 -> 0.34 ms per step at 32 px; c2
@@ -1413,6 +1416,15 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
     const bool valid = u < nu && v < nv;
     const size_t rid = ((size_t)a * nv + v) * nu + u;
     const int e = valid ? ld_stream(entry + rid) : -1;
+#if TRACE_EMPTY_EXIT
+    // a block none of whose rays enters the mesh (outside the silhouette:
+    // ~half of c3's blocks) writes its zero projections and leaves before
+    // the axis vote and the statistics reductions
+    if (!__syncthreads_or(e >= 0)) {
+        if (!BACK && valid) st_stream(proj + rid, 0.f);
+        return;
+    }
+#endif
 
     unsigned n_cross = 0, n_exact = 0, n_lost = 0, n_stuck = 0;
     double sum = 0.0;
