@@ -1,8 +1,8 @@
 #!/usr/bin/env python
 """Small workload touching every kernel family, for compute-sanitizer runs:
-exact walker (forward/backward, degenerate c1 + lattice + ball), both entry
-finders, the paper-faithful MT walker, the permutes.  Exits non-zero on any
-error or parity break."""
+exact walker (forward/backward, degenerate c1 + lattice + ball), the three
+entry finders, the paper-faithful MT walker, the permutes, plans (device and
+host buffers, f64 accumulation).  Exits non-zero on any error."""
 import os
 import sys
 
@@ -21,12 +21,20 @@ from workloads import meshes as M  # noqa: E402
 def run(mesh, geom, mu, y):
     tm = T.TetMesh.from_mesh(mesh)
     mu_d, y_d = torch.from_numpy(mu).cuda(), torch.from_numpy(y).cuda()
-    for opts in (None, T.options(entry=T.TET_ENTRY_BVH), T.options(T.TET_TRAVERSE_MT_F64),
-                 T.options(T.TET_TRAVERSE_MT_F32)):
+    for opts in (None, T.options(entry=T.TET_ENTRY_BVH), T.options(entry=T.TET_ENTRY_RTREE),
+                 T.options(T.TET_TRAVERSE_MT_F64), T.options(T.TET_TRAVERSE_MT_F32)):
         p, st = tm.project(geom, mu_d, stats=True, opts=opts)
         x, st2 = tm.backproject(geom, y_d, stats=True, opts=opts)
         if opts is None:
             assert st["lost"] == st["stuck"] == st["entry_conflicts"] == 0, st
+    with tm.plan(geom) as pl:
+        p2 = pl.project(mu_d)
+        pl.backproject(y_d)
+        pl.backproject_f64(y_d)
+        T.tet_plan_project(pl.handle, mu, np.zeros(geom.n_rays, np.float32))
+        T.tet_plan_backproject(pl.handle, y, np.zeros(mesh.n_tets, np.float32))
+        torch.cuda.synchronize()
+    assert torch.equal(p2, tm.project(geom, mu_d))
     torch.cuda.synchronize()
 
 
