@@ -65,6 +65,11 @@ typedef __int128 i128;
 #ifndef TRACE_EMPTY_EXIT
 #define TRACE_EMPTY_EXIT 1
 #endif
+// early exit and shear-axis vote per WARP instead of per block: no block
+// barrier at the start of the walk (c3 1.671e11 -> 1.678e11; 0 = per block)
+#ifndef TRACE_WARP_VOTE
+#define TRACE_WARP_VOTE 1
+#endif
 // footprints of at most this many pixels go to entry_small_kernel (thread
 // per item); 0 sends every item to the warp raster.  c4a (36,300 hull faces
 // of ~1 px at lattice pitch): entry 0.88 -> 0.34 ms per step at 32 px; c2
@@ -1416,7 +1421,12 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
     const bool valid = u < nu && v < nv;
     const size_t rid = ((size_t)a * nv + v) * nu + u;
     const int e = valid ? ld_stream(entry + rid) : -1;
-#if TRACE_EMPTY_EXIT
+#if TRACE_WARP_VOTE
+    if (!__any_sync(0xffffffffu, e >= 0)) {   // no ray of this warp enters the mesh
+        if (!BACK && valid) st_stream(proj + rid, 0.f);
+        return;
+    }
+#elif TRACE_EMPTY_EXIT
     // a block none of whose rays enters the mesh (outside the silhouette:
     // ~half of c3's blocks) writes its zero projections and leaves before
     // the axis vote and the statistics reductions
@@ -1428,13 +1438,19 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
 
     unsigned n_cross = 0, n_exact = 0, n_lost = 0, n_stuck = 0;
     double sum = 0.0;
-    // Block-uniform shear axis: the tile's centre ray decides; every ray of the
-    // block must be dominated (|D_k| >= max|D|/2) by that axis with the same
-    // sign (block vote), else the generic per-ray frame (variant 6) is used.
+    // Warp-uniform shear axis (block-uniform with TRACE_WARP_VOTE = 0): the
+    // warp tile's centre ray decides; every ray of the warp must be dominated
+    // (|D_k| >= max|D|/2) by that axis with the same sign (warp vote), else the
+    // generic per-ray frame (variant 6) is used.
     int ax = 6;
     {
+#if TRACE_WARP_VOTE
+        const int uc = min(bx * BX * tw + (w % BX) * tw + tw / 2, nu - 1);   // the warp tile's centre
+        const int vc = min(by * BY * th + (w / BX) * th + th / 2, nv - 1);
+#else
         const int uc = min(bx * BX * tw + BX * tw / 2, nu - 1);
         const int vc = min(by * BY * th + BY * th / 2, nv - 1);
+#endif
         const RayPts rc = ray_points(ang[a], beam, uc, vc);
         const long long cx = rc.px - rc.ox, cy = rc.py - rc.oy, cz = rc.pz - rc.oz;
         const long long ax_ = cx < 0 ? -cx : cx, ay_ = cy < 0 ? -cy : cy, az_ = cz < 0 ? -cz : cz;
@@ -1449,7 +1465,11 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
             const long long m = max(dx < 0 ? -dx : dx, max(dy < 0 ? -dy : dy, dz < 0 ? -dz : dz));
             ok = (dk < 0) == (dkc < 0) && 2 * adk >= m;
         }
+#if TRACE_WARP_VOTE
+        if (__all_sync(0xffffffffu, ok)) ax = 2 * kc + (dkc < 0 ? 1 : 0);
+#else
         if (__syncthreads_and(ok)) ax = 2 * kc + (dkc < 0 ? 1 : 0);
+#endif
         // parallel beam: the uniform shear was made for the angle's axis variant
         if (beam != TET_BEAM_CONE && ax != (int)UF.f[a].q[2]) ax = 6;
     }
