@@ -65,6 +65,13 @@ typedef __int128 i128;
 #ifndef TRACE_EMPTY_EXIT
 #define TRACE_EMPTY_EXIT 1
 #endif
+#ifndef TRACE_HEAVY_KEEP_RAY
+#define TRACE_HEAVY_KEEP_RAY 1
+#endif
+// exact-heavy scans on the FT16 walk too (1) or on the record walk (0)
+#ifndef TRACE_HEAVY_FT
+#define TRACE_HEAVY_FT 0
+#endif
 // early exit and shear-axis vote per WARP instead of per block: no block
 // barrier at the start of the walk (c3 1.671e11 -> 1.678e11; 0 = per block)
 #ifndef TRACE_WARP_VOTE
@@ -237,6 +244,24 @@ __device__ __noinline__ unsigned exact_neg_here(const int4* __restrict__ vtx,
         if (!(mask >> k & 1u)) continue;
         const int4 B = __ldg(vtx + ids[k]);
         const int sg = sos_side(A.x, A.y, A.z, B.x, B.y, B.z, r.ox, r.oy, r.oz, r.px, r.py, r.pz);
+        neg = (neg & ~(1u << k)) | (sg < 0 ? 1u << k : 0u);
+    }
+    return neg;
+}
+
+// The exact-heavy walk shape (128 registers) keeps its ray's grid points and
+// passes them (TRACE_HEAVY_KEEP_RAY): no pixel decode, AngleGeom load or
+// ray_points per call.
+__device__ __noinline__ unsigned exact_neg_ray(const int4* __restrict__ vtx, long long ox,
+                                               long long oy, long long oz, long long px,
+                                               long long py, long long pz, unsigned mask,
+                                               unsigned neg, int iap, int id0, int id1, int id2) {
+    const int4 A = __ldg(vtx + iap);
+    const int ids[3] = {id0, id1, id2};
+    for (int k = 0; k < 3; ++k) {
+        if (!(mask >> k & 1u)) continue;
+        const int4 B = __ldg(vtx + ids[k]);
+        const int sg = sos_side(A.x, A.y, A.z, B.x, B.y, B.z, ox, oy, oz, px, py, pz);
         neg = (neg & ~(1u << k)) | (sg < 0 ? 1u << k : 0u);
     }
     return neg;
@@ -1178,7 +1203,9 @@ __device__ __forceinline__ void walk_ray(const UniFrame& U, const int4* __restri
             if (any_abs_le(p0, p1, p2, tau)) {
                 const unsigned mask = (fabs(p0) <= tau ? 1u : 0u) | (fabs(p1) <= tau ? 2u : 0u) |
                                       (fabs(p2) <= tau ? 4u : 0u);
-                if (BACK ? TRACE_BWD_ONECALL : TRACE_EXACT_ONECALL) {
+                if (TRACE_HEAVY_KEEP_RAY && !LATE) {   // the exact-heavy shape (early gathers)
+                    neg = exact_neg_ray(vtx, r.ox, r.oy, r.oz, r.px, r.py, r.pz, mask, neg, iap, id0, id1, id2);
+                } else if (BACK ? TRACE_BWD_ONECALL : TRACE_EXACT_ONECALL) {
                     neg = exact_neg_here<BX, BY, BAND>(vtx, ang, beam, nu, tw_log, mask, neg, iap, id0, id1, id2);
                 } else {
                     const unsigned m = neg;
@@ -1282,7 +1309,7 @@ __device__ __forceinline__ RayPts ft_scaled(RayPts r) {
     return r;
 }
 
-template <bool BACK, int AX, int UNI, int BX, int BY, bool BAND>
+template <bool BACK, int AX, int UNI, int BX, int BY, bool BAND, bool KEEP>
 __device__ __forceinline__ void walk_ray_ft(const UniFrame& Ug, const int4* __restrict__ tag,
                                             const int4* __restrict__ tnode,
                                             const int4* __restrict__ vtx,
@@ -1339,7 +1366,11 @@ __device__ __forceinline__ void walk_ray_ft(const UniFrame& Ug, const int4* __re
         if (any_abs_le(p0, p1, p2, tau)) {
             const unsigned mask = (fabs(p0) <= tau ? 1u : 0u) | (fabs(p1) <= tau ? 2u : 0u) |
                                   (fabs(p2) <= tau ? 4u : 0u);
-            if (BACK ? TRACE_BWD_ONECALL : TRACE_EXACT_ONECALL) {
+            if (TRACE_HEAVY_KEEP_RAY && KEEP) {   // exact-heavy shape: the ray's (unscaled) grid points
+                neg = exact_neg_ray(vtx, r.ox >> kFtShift, r.oy >> kFtShift, r.oz >> kFtShift,
+                                    r.px >> kFtShift, r.py >> kFtShift, r.pz >> kFtShift, mask,
+                                    neg, iap, id0, id1, id2);
+            } else if (BACK ? TRACE_BWD_ONECALL : TRACE_EXACT_ONECALL) {
                 neg = exact_neg_here<BX, BY, BAND>(vtx, ang, beam, nu, tw_log, mask, neg, iap, id0, id1, id2);
             } else {
                 const unsigned m = neg;
@@ -1476,7 +1507,7 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB) trace_kernel(const int4* _
     const UniFrame& U = UF.f[a];
     if (e >= 0) {
 #define WALK(AXV, UNI) do { \
-    if (FT) walk_ray_ft<BACK, AXV, UNI, BX, BY, BAND>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tile_code, rmax, g, \
+    if (FT) walk_ray_ft<BACK, AXV, UNI, BX, BY, BAND, !LATE>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tile_code, rmax, g, \
                                       max_steps, nverts, e, rid, mu, y, acc, sum, n_cross, n_exact, n_lost, n_stuck); \
     else walk_ray<BACK, AXV, UNI, BX, BY, LATE, BAND>(U, rec, tnode, vtx, ang, beam, a, u, v, nu, tile_code, rmax, g, \
                                       max_steps, \
@@ -1937,7 +1968,7 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     static thread_local UniFrames U;   // 10 KB: copied into the launch parameters
     // FT16 walk (coordinates x64), except for exact-heavy scans: there the
     // rec walk's shape measured faster (c4a 9.32e9 vs 8.98e9 crossings/s)
-    const bool ft = m.tag16 != nullptr && !HEAVY;
+    const bool ft = m.tag16 != nullptr && (!HEAVY || TRACE_HEAVY_FT);
     make_uni_frames(m, c, U, ft ? (double)(1 << kFtShift) : 1.0);
     auto kern = ft ? (big ? trace_kernel<BACK, S::BX, S::BY, S::MINB_FT, S::LATE, true, true>
                           : trace_kernel<BACK, S::BX, S::BY, S::MINB_FT, S::LATE, false, true>)
