@@ -1896,8 +1896,11 @@ template <> struct TraceShape<false, true> {
     static constexpr int BX = 2, BY = 2, MINB = TRACE_HEAVY_FWD_MINB, MINB_FT = MINB;
     static constexpr bool LATE = false;
 };
+#ifndef TRACE_HEAVY_BWD_MINB
+#define TRACE_HEAVY_BWD_MINB 4
+#endif
 template <> struct TraceShape<true, true> {
-    static constexpr int BX = 2, BY = 2, MINB = 4, MINB_FT = MINB;
+    static constexpr int BX = 2, BY = 2, MINB = TRACE_HEAVY_BWD_MINB, MINB_FT = MINB;
     static constexpr bool LATE = false;
 };
 
