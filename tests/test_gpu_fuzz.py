@@ -82,3 +82,28 @@ def test_random_scans_paper_mode_match_mt_oracle(seed):
     for k in ("rays_hit", "crossings", "lost", "stuck", "escalations"):
         assert st[k] == ost[k], (k, st, ost)
     np.testing.assert_array_equal(p.cpu().numpy().ravel(), q.astype(np.float32).ravel())
+
+
+@pytest.mark.parametrize("seed", range(0, 48, 4))
+def test_random_scans_through_plans(seed):
+    """The same random scans through a plan (entry map built once, each entry
+    finder in turn): bit-identical projections and equal statistics to the
+    plan-less calls, backprojections equal up to the atomics' order."""
+    import torch
+
+    from paper_1908_06909_b200 import tetproj as T
+    mesh, geom, mu, y = _case(seed)
+    entry = [T.TET_ENTRY_RASTER, T.TET_ENTRY_BVH, T.TET_ENTRY_RTREE][(seed // 4) % 3]
+    opts = T.options(entry=entry)
+    tm = T.TetMesh.from_mesh(mesh)
+    mu_d, y_d = torch.from_numpy(mu).cuda(), torch.from_numpy(y).cuda()
+    p0, s0 = tm.project(geom, mu_d, stats=True, opts=opts)
+    x0, t0 = tm.backproject(geom, y_d, stats=True, opts=opts)
+    with tm.plan(geom, opts) as pl:
+        p1, s1 = pl.project(mu_d, stats=True)
+        x1, t1 = pl.backproject(y_d, stats=True)
+        torch.cuda.synchronize()
+    assert torch.equal(p0, p1)
+    for k in ("rays_hit", "crossings", "lost", "stuck", "exact_fallbacks", "entry_conflicts"):
+        assert s0[k] == s1[k] and t0[k] == t1[k], (k, s0, s1, t0, t1)
+    np.testing.assert_allclose(x1.cpu().numpy(), x0.cpu().numpy(), rtol=2e-7, atol=1e-30)
