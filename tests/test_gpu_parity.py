@@ -534,3 +534,35 @@ def test_backproject_accumulate_device():
     _, xr, _, _ = U.run_oracle(w.mesh, w.geom, w.mu, w.y)
     be = U.back_errors(x.cpu().numpy().astype(np.float64) / 2, xr)
     assert be.max() <= U.BACK_TOL, be.max()
+
+
+def test_large_single_angle_detector_sampled():
+    """Maximum-size edge case: ONE angle of a 4099 x 4097 detector (16.8 M
+    rays in a single angle chunk: the largest grid of one walk launch, ragged
+    in both directions), through a plan; sampled rays vs the oracle one by
+    one, every tet's backprojection of the sampled rays, and the total-sum
+    identity."""
+    import torch
+
+    from oracle import tetref as O
+    from paper_1908_06909_b200 import tetproj as T
+    w = CF.workload("c2")
+    R = 1.0
+    geom = G.circular_cone([0.37], 4 * R, 8 * R, 4099, 4097, 4.6 * R / 4099, 4.6 * R / 4097)
+    tm = T.TetMesh.from_mesh(w.mesh)
+    mu = torch.from_numpy(w.mu).cuda()
+    with tm.plan(geom) as pl:
+        p, st = pl.project(mu, stats=True)
+        ones_r = torch.ones(geom.n_rays, device="cuda")
+        colsum = pl.backproject(ones_r).double().sum().item()
+        rowsum = pl.project(torch.ones_like(mu)).double().sum().item()
+    assert st["rays"] == geom.n_rays and st["lost"] == st["stuck"] == st["entry_conflicts"] == 0
+    assert st["rays_hit"] > 0.5 * geom.n_rays
+    assert abs(rowsum - colsum) / rowsum <= U.ADJ_TOL
+    rng = np.random.default_rng(11)
+    ids = np.sort(rng.choice(geom.n_rays, 2000, replace=False))
+    om = O.OracleMesh.from_mesh(w.mesh)
+    pr, _ = O.project(om, geom, w.mu.astype(np.float64), ray_ids=ids)
+    fe = U.fwd_errors(p.cpu().numpy().ravel()[ids].astype(np.float64), pr, w.mu, w.mesh)
+    assert fe.max() <= U.FWD_TOL
+    _sampled_backprojection_check(tm, geom, w.mesh, om, ids, min_nonzero=500)
