@@ -1879,28 +1879,37 @@ template <bool BACK, bool HEAVY> struct TraceShape;
 #ifndef TRACE_FT_BWD_MINB
 #define TRACE_FT_BWD_MINB 10
 #endif
+// ... and of the band-ordered backward (meshes beyond half the L2, c5): 8
+// blocks at 64 registers (c5 backward 545 ms at 10, 530 at 9, 526 at 8, 558
+// at 7, 568 at 6; c3's angle-ordered backward stays at 10: 30.4 vs 30.9 ms
+// at 9), profiles/README.md
+#ifndef TRACE_FT_BWD_BAND_MINB
+#define TRACE_FT_BWD_BAND_MINB 8
+#endif
 template <> struct TraceShape<false, false> {
     static constexpr int BX = TRACE_FWD_BX, BY = TRACE_FWD_BY, MINB = TRACE_FWD_MINB;
-    static constexpr int MINB_FT = TRACE_FWD_MINB;
+    static constexpr int MINB_FT = TRACE_FWD_MINB, MINB_FT_BAND = MINB_FT;
     static constexpr bool LATE = TRACE_FWD_LATE_LOADS;
 };
 template <> struct TraceShape<true, false> {
     static constexpr int BX = TRACE_BWD_BX, BY = TRACE_BWD_BY, MINB = TRACE_BWD_MINB;
-    static constexpr int MINB_FT = TRACE_FT_BWD_MINB;
+    static constexpr int MINB_FT = TRACE_FT_BWD_MINB, MINB_FT_BAND = TRACE_FT_BWD_BAND_MINB;
     static constexpr bool LATE = TRACE_BWD_LATE_LOADS;
 };
 #ifndef TRACE_HEAVY_FWD_MINB
 #define TRACE_HEAVY_FWD_MINB 4
 #endif
 template <> struct TraceShape<false, true> {
-    static constexpr int BX = 2, BY = 2, MINB = TRACE_HEAVY_FWD_MINB, MINB_FT = MINB;
+    static constexpr int BX = 2, BY = 2, MINB = TRACE_HEAVY_FWD_MINB, MINB_FT = MINB,
+                         MINB_FT_BAND = MINB;
     static constexpr bool LATE = false;
 };
 #ifndef TRACE_HEAVY_BWD_MINB
 #define TRACE_HEAVY_BWD_MINB 4
 #endif
 template <> struct TraceShape<true, true> {
-    static constexpr int BX = 2, BY = 2, MINB = TRACE_HEAVY_BWD_MINB, MINB_FT = MINB;
+    static constexpr int BX = 2, BY = 2, MINB = TRACE_HEAVY_BWD_MINB, MINB_FT = MINB,
+                         MINB_FT_BAND = MINB;
     static constexpr bool LATE = false;
 };
 
@@ -1973,7 +1982,7 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     // rec walk's shape measured faster (c4a 9.32e9 vs 8.98e9 crossings/s)
     const bool ft = m.tag16 != nullptr && (!HEAVY || TRACE_HEAVY_FT);
     make_uni_frames(m, c, U, ft ? (double)(1 << kFtShift) : 1.0);
-    auto kern = ft ? (big ? trace_kernel<BACK, S::BX, S::BY, S::MINB_FT, S::LATE, true, true>
+    auto kern = ft ? (big ? trace_kernel<BACK, S::BX, S::BY, S::MINB_FT_BAND, S::LATE, true, true>
                           : trace_kernel<BACK, S::BX, S::BY, S::MINB_FT, S::LATE, false, true>)
                    : (big ? trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, true, false>
                           : trace_kernel<BACK, S::BX, S::BY, S::MINB, S::LATE, false, false>);
