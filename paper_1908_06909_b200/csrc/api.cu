@@ -621,10 +621,11 @@ tet_status tet_mesh_create(const double* verts, int64_t n_verts, const int32_t* 
             int max_persist = 0, max_window = 0;
             cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
             cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
-            const size_t rec_bytes = (size_t)H.nt * 32;
+            // the walked table: FT16 tags (64 B per tet) or the records (32 B)
+            const size_t table_bytes = (size_t)H.nt * (H.ft16 ? 64 : 32);
             if (max_persist > 0 && max_window > 0) {
                 cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
-                m->dev.l2_window_bytes = std::min(rec_bytes, (size_t)max_window);
+                m->dev.l2_window_bytes = std::min(table_bytes, (size_t)max_window);
                 m->dev.l2_hit_ratio = std::min(1.0, (double)max_persist / (double)m->dev.l2_window_bytes);
             }
         }

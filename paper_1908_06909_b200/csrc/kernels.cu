@@ -2001,7 +2001,7 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    attr[0].val.accessPolicyWindow.base_ptr = (void*)m.rec;
+    attr[0].val.accessPolicyWindow.base_ptr = (void*)rec_or_tag;   // the table this walk gathers
     attr[0].val.accessPolicyWindow.num_bytes = m.l2_window_bytes;
     attr[0].val.accessPolicyWindow.hitRatio = (float)m.l2_hit_ratio;
     attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
