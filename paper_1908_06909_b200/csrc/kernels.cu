@@ -96,6 +96,10 @@ typedef __int128 i128;
 // angles per band group of the backward walk on L2-exceeding meshes: 2 for
 // round 1's record walk, 4 for the FT16 walk (c5 backward 558 -> 548 ms;
 // 1: 591, 8: 552, 16: 558), profiles/README.md
+// forward: all of a launch's angles per band (plain band order)
+#ifndef TRACE_FWD_BAND_GROUP
+#define TRACE_FWD_BAND_GROUP (1 << 20)
+#endif
 #ifndef TRACE_BWD_BAND_GROUP
 #define TRACE_BWD_BAND_GROUP 4
 #endif
@@ -1975,7 +1979,7 @@ static void launch_trace(const DevMesh& m, const LaunchChunk& c, const int* entr
     // band order: c3 backward 34.8 -> 52.9 ms).  L2-resident meshes keep
     // angle order (c3 forward 27.1 -> 27.3 ms with bands).
     const bool big = TRACE_BAND_ORDER && (size_t)m.nt * TRACE_BAND_BYTES_PER_TET > l2_bytes() / 2;
-    const int group = big ? (BACK ? TRACE_BWD_BAND_GROUP : 1 << 20) : 0;
+    const int group = big ? (BACK ? TRACE_BWD_BAND_GROUP : TRACE_FWD_BAND_GROUP) : 0;
     const int tile_code = twl | group << 4;
     static thread_local UniFrames U;   // 10 KB: copied into the launch parameters
     // FT16 walk (coordinates x64), except for exact-heavy scans: there the
