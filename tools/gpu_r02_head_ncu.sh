@@ -8,7 +8,7 @@ ncu -i $R/c3.ncu-rep --page source --csv --print-source sass > $R/c3_src.csv 2>/
 timeout 1500 ncu --set full --clock-control none -k regex:trace_kernel -s 0 -c 1 -o $R/c5f -f python bench.py --config c5 --no-cpu-baseline --e2e-steps 0 --steps 1 --warmup 3 > gpurun_out/head_ncu_c5_fwd.log 2>&1; echo "ncu c5 fwd $?"
 python tools/ncu_summary.py $R/c5f.ncu-rep "c5 forward walk (FT16, band order), launch 0: 64 of 720 angles" > gpurun_out/head_ncu_c5_fwd_summary.json
 timeout 1500 ncu --set full --clock-control none --kernel-name-base demangled -k 'regex:trace_kernel<.bool.1' -s 0 -c 1 -o $R/c5b -f python bench.py --config c5 --no-cpu-baseline --e2e-steps 0 --steps 1 --warmup 3 > gpurun_out/head_ncu_c5_back.log 2>&1; echo "ncu c5 back $?"
-python tools/ncu_summary.py $R/c5b.ncu-rep "c5 backward walk (FT16, 10 blocks/SM, bands of 4 angles), launch 0: 64 of 720 angles" > gpurun_out/head_ncu_c5_back_summary.json
+python tools/ncu_summary.py $R/c5b.ncu-rep "c5 backward walk (FT16, band order: 8 blocks/SM, bands of 4 angles), launch 0: 64 of 720 angles" > gpurun_out/head_ncu_c5_back_summary.json
 for cfg in c2 c4b; do
   timeout 900 ncu --set full --clock-control none -k regex:trace_kernel -s 0 -c 1 -o $R/${cfg}f -f python bench.py --config $cfg --no-cpu-baseline --e2e-steps 0 --steps 1 --warmup 3 > gpurun_out/head_ncu_${cfg}_fwd.log 2>&1; echo "ncu $cfg fwd $?"
   python tools/ncu_summary.py $R/${cfg}f.ncu-rep "$cfg forward walk (FT16), launch 0 (all angles)" > gpurun_out/head_ncu_${cfg}_fwd_summary.json
