@@ -48,12 +48,12 @@ def test_ncu_traffic_per_config():
     sys.path.insert(0, ROOT)
     import bench
     table = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-    for cfg in ("c2", "c3", "c4b", "c5"):
+    for cfg in ("c2", "c3", "c4b", "c5", "c4a"):
         for k in ("forward", "backward"):
             per = table[cfg][k]["dram_bytes_per_crossing"]
             assert 0 < per < 96            # below the no-reuse sector traffic
             assert bench.ncu_traffic(cfg, k, 1e9) == pytest.approx(per * 1e9)
-    assert bench.ncu_traffic("c4a", "backward", 1e9) is None   # no capture: null, not a guess
+    assert bench.ncu_traffic("c1", "backward", 1e9) is None    # no capture: null, not a guess
 
 
 def test_gpus_flag_fails_loudly_without_the_gpus():
@@ -92,7 +92,7 @@ def test_roofline_fields_recompute_from_profiles():
     assert rl["frac"] == pytest.approx(want / rl["peak"])
     assert rl["hbm"]["achieved"] == pytest.approx(36 * 3.0e9 / 20e-3 / 1e9)
     # no capture for the config: the HBM view, labelled as such
-    rl2 = bench.roofline("c4a", "forward", 1e9, 10.0, 1965.0)
+    rl2 = bench.roofline("c1", "forward", 1e9, 10.0, 1965.0)
     assert rl2["bound"] == "hbm" and rl2["unit"] == "GB/s"
 
 

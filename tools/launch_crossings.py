@@ -2,7 +2,7 @@
 """Crossings of the walk launches that tools/gpu_r02_head_ncu.sh captures
 (the first launch of each direction in bench.py's untimed statistics calls):
 c3 launch 0 = angles [0, 256) (2^26 rays per launch), c5 launch 0 = [0, 64),
-c2 / c4b = all angles.  Writes one JSON object to stdout."""
+c2 / c4b / c4a = all angles.  Writes one JSON object to stdout."""
 import json
 import os
 import sys
@@ -16,7 +16,7 @@ import torch  # noqa: E402
 from paper_1908_06909_b200 import tetproj as T  # noqa: E402
 from workloads import configs as CF  # noqa: E402
 
-LAUNCH0 = {"c3": 256, "c5": 64, "c2": None, "c4b": None}
+LAUNCH0 = {"c3": 256, "c5": 64, "c2": None, "c4b": None, "c4a": None}
 
 
 def main():

@@ -6,8 +6,9 @@ the captured launches (tools/launch_crossings.py):
   python tools/ncu_to_profiles.py PREFIX crossings.json "source note"
 
 PREFIX_c3_summary.json holds [c3 forward launch 0, c3 forward launch 1,
-c3 backward launch 0]; PREFIX_{c5,c2,c4b}_{fwd,back}_summary.json one
-launch each."""
+c3 backward launch 0]; PREFIX_{c5,c2,c4b,c4a}_{fwd,back}_summary.json one
+launch each (c4a, when present: the exact-heavy shape its timed steps run,
+tools/gpu_r02_c4a_ncu.sh)."""
 import json
 import os
 import sys
@@ -24,6 +25,12 @@ def scaled(s):
     return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit]
 
 
+def ms(s):
+    v, unit = str(s).split()[:2]
+    return float(v) * {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0,
+                       "msecond": 1.0, "s": 1e3, "second": 1e3}[unit]
+
+
 def entry(k, crossings):
     return {
         "warp_inst_per_crossing": round(num(k["smsp__inst_executed.sum"]) / crossings, 4),
@@ -34,7 +41,7 @@ def entry(k, crossings):
         "red_l2_sectors_per_crossing": round(num(k["lts__t_sectors_srcunit_tex_op_red.sum"]) / crossings, 4),
         "local_loads_per_crossing": round(num(k["smsp__sass_inst_executed_op_local_ld.sum"]) / crossings, 4),
         "registers": int(num(k["launch__registers_per_thread"])),
-        "kernel_ms_ncu": num(k["gpu__time_duration.sum"]),
+        "kernel_ms_ncu": ms(k["gpu__time_duration.sum"]),
         "crossings": crossings,
     }
 
@@ -46,7 +53,9 @@ def main(prefix, cross_path, note):
                           "launch / its crossings (ncu flushes caches before each captured "
                           "kernel, so the cold read of the tag table is included), same "
                           "captures as profiles/ncu_issue.json"}
-    for cfg in ("c3", "c5", "c2", "c4b"):
+    for cfg in ("c3", "c5", "c2", "c4b", "c4a"):
+        if cfg not in cross or (cfg != "c3" and not os.path.exists(f"{prefix}_{cfg}_fwd_summary.json")):
+            continue
         c = cross[cfg]["crossings"]
         if cfg == "c3":
             ks = json.load(open(f"{prefix}_c3_summary.json"))
