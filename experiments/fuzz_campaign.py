@@ -1,0 +1,50 @@
+#!/usr/bin/env python
+"""A wider randomized parity campaign than tests/test_gpu_fuzz.py (same
+generator, seeds [first, first + n)): random small meshes on a coarse
+lattice (rays through vertices / edges / faces are common) under random cone
+/ parallel / lattice-aligned scans, each entry finder in turn and both exact
+walks, every case element by element against the CPU oracle with the
+north-star tolerances (tests/gpu_util.check_parity).  Prints one JSON line:
+cases, failures (seed + message), totals of rays, crossings and exact
+fallbacks.
+
+  python experiments/fuzz_campaign.py [first_seed] [n]
+"""
+import json
+import os
+import sys
+import traceback
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_1908_06909_b200 import tetproj as T  # noqa: E402
+from tests import gpu_util as U  # noqa: E402
+from tests.test_gpu_fuzz import _case  # noqa: E402
+
+
+def main(first=100, n=400):
+    fails, rays, cross, exact = [], 0, 0, 0
+    for seed in range(first, first + n):
+        mesh, geom, mu, y = _case(seed)
+        entry = [T.TET_ENTRY_RASTER, T.TET_ENTRY_BVH, T.TET_ENTRY_RTREE][seed % 3]
+        walker = "rec" if seed % 5 == 4 else None
+        if walker:
+            os.environ["TETPROJ_WALKER"] = walker
+        try:
+            r = U.check_parity(mesh, geom, mu, y, opts=T.options(entry=entry))
+            rays += r["stats"]["rays"]
+            cross += r["stats"]["crossings"]
+            exact += r["stats"]["exact_fallbacks"]
+        except Exception as e:   # noqa: BLE001 -- record and continue
+            fails.append({"seed": seed, "error": repr(e)[:300],
+                          "where": traceback.format_exc().splitlines()[-3:]})
+        finally:
+            os.environ.pop("TETPROJ_WALKER", None)
+    print(json.dumps({"first_seed": first, "cases": n, "failures": fails, "rays": rays,
+                      "crossings": cross, "exact_fallbacks": exact}))
+
+
+if __name__ == "__main__":
+    a = [int(x) for x in sys.argv[1:3]]
+    main(*a)
