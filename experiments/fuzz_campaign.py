@@ -9,6 +9,7 @@ cases, failures (seed + message), totals of rays, crossings and exact
 fallbacks.
 
   python experiments/fuzz_campaign.py [first_seed] [n]
+  python experiments/fuzz_campaign.py mt first_seed n   # the paper's walk vs the MT oracle
 """
 import json
 import os
@@ -21,6 +22,39 @@ sys.path.insert(0, ROOT)
 from paper_1908_06909_b200 import tetproj as T  # noqa: E402
 from tests import gpu_util as U  # noqa: E402
 from tests.test_gpu_fuzz import _case  # noqa: E402
+
+
+def mt_case(seed):
+    """The paper's Alg. 1/2 walk (fp64 for even seeds, fp32 for odd) vs the
+    MT oracle: bit-identical projections, equal crossing / lost / stuck /
+    escalation counts (tests/test_gpu_fuzz.py::test_random_scans_paper_mode_match_mt_oracle)."""
+    import numpy as np
+    import torch
+
+    from oracle import tetref as O
+    mesh, geom, mu, y = _case(seed)
+    single = bool(seed % 2)
+    tm = T.TetMesh.from_mesh(mesh)
+    mode = T.TET_TRAVERSE_MT_F32 if single else T.TET_TRAVERSE_MT_F64
+    p, st = tm.project(geom, torch.from_numpy(mu).cuda(), stats=True, opts=T.options(mode))
+    q, ost = O.mt_project(O.OracleMesh.from_mesh(mesh), geom, mu.astype(np.float64), single=single)
+    for k in ("rays_hit", "crossings", "lost", "stuck", "escalations"):
+        assert st[k] == ost[k], (k, st, ost)
+    np.testing.assert_array_equal(p.cpu().numpy().ravel(), q.astype(np.float32).ravel())
+    return st
+
+
+def main_mt(first, n):
+    fails, lost, esc = [], 0, 0
+    for seed in range(first, first + n):
+        try:
+            st = mt_case(seed)
+            lost += st["lost"] + st["stuck"]
+            esc += st["escalations"]
+        except Exception as e:   # noqa: BLE001
+            fails.append({"seed": seed, "error": repr(e)[:300]})
+    print(json.dumps({"mode": "mt", "first_seed": first, "cases": n, "failures": fails,
+                      "paper_walk_lost_or_stuck": lost, "escalations": esc}))
 
 
 def main(first=100, n=400):
@@ -46,5 +80,7 @@ def main(first=100, n=400):
 
 
 if __name__ == "__main__":
-    a = [int(x) for x in sys.argv[1:3]]
-    main(*a)
+    if sys.argv[1:2] == ["mt"]:
+        main_mt(*[int(x) for x in sys.argv[2:4]])
+    else:
+        main(*[int(x) for x in sys.argv[1:3]])
