@@ -9,7 +9,8 @@ cases, failures (seed + message), totals of rays, crossings and exact
 fallbacks.
 
   python experiments/fuzz_campaign.py [first_seed] [n]
-  python experiments/fuzz_campaign.py mt first_seed n   # the paper's walk vs the MT oracle
+  python experiments/fuzz_campaign.py mt first_seed n      # the paper's walk vs the MT oracle
+  python experiments/fuzz_campaign.py medium first_seed n  # 1e3-1e5-tet meshes
 """
 import json
 import os
@@ -57,6 +58,62 @@ def main_mt(first, n):
                       "paper_walk_lost_or_stuck": lost, "escalations": esc}))
 
 
+def medium_case(seed):
+    """Medium meshes (ball Delaunay h in [0.15, 0.35]; jittered lattices n in
+    [4, 14] with jitter 1e-4 / 1e-3 / 0.05 / 0.2 h -- slivers; graded boxes of
+    2-8 k interior points; exact Kuhn lattices n in [2, 8] -- vertex and edge
+    degeneracies) under random cone / parallel scans of 8-48^2 pixels, 1-4
+    angles."""
+    import numpy as np
+
+    from workloads import geometry as G
+    from workloads import meshes as M
+    rng = np.random.default_rng(50_000 + seed)
+    kind = seed % 4
+    if kind == 0:
+        mesh = M.ball_mesh(h=float(rng.uniform(0.15, 0.35)), seed=seed)
+    elif kind == 1:
+        mesh = M.jittered_lattice_mesh(int(rng.integers(4, 15)),
+                                       float([1e-4, 1e-3, 0.05, 0.2][(seed // 4) % 4]), seed)
+    elif kind == 3:   # exact Kuhn lattice: rays through vertices and edges
+        mesh = M.kuhn_lattice(int(rng.integers(2, 9)))
+    else:
+        mesh = M.graded_box_mesh(int(rng.integers(2000, 8000)), seed=seed, per_edge=2, per_face=6)
+    R = float(np.linalg.norm(mesh.verts, axis=1).max())
+    n_u, n_v = int(rng.integers(8, 49)), int(rng.integers(8, 49))
+    ang = rng.uniform(0, 2 * np.pi, int(rng.integers(1, 5)))
+    if rng.uniform() < 0.6:
+        dso = R * rng.uniform(1.5, 4)
+        dsd = dso + R * rng.uniform(1.5, 4)
+        mag = dsd / dso
+        geom = G.circular_cone(ang, dso, dsd, n_u, n_v, 2.4 * R * mag / n_u, 2.4 * R * mag / n_v,
+                               off_u=rng.uniform(-1, 1), off_v=rng.uniform(-1, 1))
+    else:
+        geom = G.circular_parallel(ang, n_u, n_v, 2.4 * R / n_u, 2.4 * R / n_v,
+                                   off_u=rng.uniform(-1, 1), off_v=rng.uniform(-1, 1))
+    mu = rng.uniform(0.3, 1.5, mesh.n_tets).astype(np.float32)
+    y = rng.uniform(0.5, 1.5, geom.n_rays).astype(np.float32)
+    return mesh, geom, mu, y
+
+
+def main_medium(first, n):
+    fails, rays, cross, exact, tets = [], 0, 0, 0, 0
+    for seed in range(first, first + n):
+        try:
+            mesh, geom, mu, y = medium_case(seed)
+            entry = [T.TET_ENTRY_RASTER, T.TET_ENTRY_BVH, T.TET_ENTRY_RTREE][(seed // 3) % 3]
+            r = U.check_parity(mesh, geom, mu, y, opts=T.options(entry=entry))
+            rays += r["stats"]["rays"]
+            cross += r["stats"]["crossings"]
+            exact += r["stats"]["exact_fallbacks"]
+            tets += mesh.n_tets
+        except Exception as e:   # noqa: BLE001
+            fails.append({"seed": seed, "error": repr(e)[:300],
+                          "where": traceback.format_exc().splitlines()[-3:]})
+    print(json.dumps({"mode": "medium", "first_seed": first, "cases": n, "failures": fails,
+                      "tets": tets, "rays": rays, "crossings": cross, "exact_fallbacks": exact}))
+
+
 def main(first=100, n=400):
     fails, rays, cross, exact = [], 0, 0, 0
     for seed in range(first, first + n):
@@ -82,5 +139,7 @@ def main(first=100, n=400):
 if __name__ == "__main__":
     if sys.argv[1:2] == ["mt"]:
         main_mt(*[int(x) for x in sys.argv[2:4]])
+    elif sys.argv[1:2] == ["medium"]:
+        main_medium(*[int(x) for x in sys.argv[2:4]])
     else:
         main(*[int(x) for x in sys.argv[1:3]])
