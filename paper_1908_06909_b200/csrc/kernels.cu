@@ -1,13 +1,20 @@
 // kernels.cu -- sm_100a kernels of libtetproj.
 //
-//   entry_setup_kernel / entry_raster_kernel
+//   entry_setup_kernel / entry_small_kernel / entry_raster_kernel
 //                     hull-entry finder: per (hull face,
 //                     angle) item, exact affine side coefficients, then an
 //                     exact test of every pixel in the face's detector
-//                     footprint; writes entry[ray] = tet<<2 | k.
-//   trace_kernel<B,M> ray walk (a4) + forward accumulate (a5, B=false) or
+//                     footprint (a thread per small item, a warp per large
+//                     one); writes entry[ray] = tet<<2 | k.  A plan
+//                     (api.cu, tet_plan_create) keeps that map for its scan.
+//   entry_bvh_kernel / entry_rtree_kernel
+//                     the per-ray alternatives (binary BVH, the paper's
+//                     R*-tree); same exact decision.
+//   trace_kernel<B,..> ray walk (a4) + forward accumulate (a5, B=false) or
 //                     backprojection scatter (a6, B=true).  Alg. 2 of the
-//                     paper with exact sign decisions.
+//                     paper with exact sign decisions:
+//                     walk_ray_ft (16-B face tags, default) or walk_ray
+//                     (32-B records: exact-heavy scans, huge meshes).
 //   mt_trace_kernel   the paper's own epsilon-MT traversal (NEXT-1 study).
 //   gather / scatter  caller order <-> internal SFC order (K4).
 //
