@@ -89,8 +89,17 @@ def dist_project(mesh, geom, mu, group=None, project=None, plan=None):
     return fn(lg, mu), sh
 
 
+def tet_shard(n_tets: int, rank: int, world: int):
+    """[lo, hi) of the caller-order tets rank `rank` holds after
+    ``dist_backproject(..., reduce="scatter")``: contiguous blocks of
+    ceil(n_tets / world)."""
+    s = -(-n_tets // world)
+    lo = min(rank * s, n_tets)
+    return lo, min(lo + s, n_tets)
+
+
 def dist_backproject(mesh, geom, y_local, group=None, backproject=None, async_op=False,
-                     precision: str = "f32", plan=None):
+                     precision: str = "f32", plan=None, reduce: str = "all"):
     """x = A^T y over all ranks: local backprojection of this rank's angles,
     then all_reduce(SUM).  ``y_local`` holds this rank's rows
     (``AngleSharding.local_stack``).  Returns the reduced per-tet tensor
@@ -101,7 +110,13 @@ def dist_backproject(mesh, geom, y_local, group=None, backproject=None, async_op
     W ranks add at most W * 2^-24 relative (R15).  "f64": each rank
     accumulates into a double tensor (tet_backproject_f64) and the double
     partial sums are reduced; the result stays float64.  ``plan``: this
-    rank's ``local_plan`` (the entry map is not recomputed)."""
+    rank's ``local_plan`` (the entry map is not recomputed).
+
+    reduce "all" (default): every rank gets the whole x (all_reduce).
+    "scatter": for a solver that shards x by tet, each rank
+    gets only its block ``tet_shard(n_tets, rank, world)`` of the sum
+    (reduce_scatter: half the all-reduce's traffic), zero-padded to
+    ceil(n_tets / world) entries."""
     import torch.distributed as dist
     sh = sharding_for(geom, group)
     lg = sh.local_geometry(geom)
@@ -116,5 +131,17 @@ def dist_backproject(mesh, geom, y_local, group=None, backproject=None, async_op
         x = mesh.backproject_f64(lg, y_local)
     else:
         x = mesh.backproject(lg, y_local)
+    if reduce == "scatter":
+        import torch
+        world = dist.get_world_size(group)
+        s = -(-x.numel() // world)
+        full = torch.zeros(s * world, dtype=x.dtype, device=x.device)
+        full[: x.numel()] = x.reshape(-1)
+        x = torch.empty(s, dtype=x.dtype, device=x.device)
+        work = dist.reduce_scatter_tensor(x, full, op=dist.ReduceOp.SUM, group=group,
+                                          async_op=async_op)
+        return (x, work) if async_op else x
+    if reduce != "all":
+        raise ValueError(f"reduce must be 'all' or 'scatter', not {reduce!r}")
     work = dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
     return (x, work) if async_op else x

@@ -43,6 +43,12 @@ def _worker(rank, world, port, out_path):
         sh = D.sharding_for(w.geom)
         y_local = sh.local_stack(w.y)
         x = D.dist_backproject(None, w.geom, y_local, backproject=backproject)
+        # reduce-scatter: this rank's contiguous block of the same sum
+        xs = D.dist_backproject(None, w.geom, y_local, backproject=backproject, reduce="scatter")
+        lo, hi = D.tet_shard(x.numel(), rank, world)
+        assert xs.numel() == -(-x.numel() // world)
+        assert torch.allclose(xs[: hi - lo], x[lo:hi], rtol=1e-12, atol=1e-12)
+        assert not xs[hi - lo:].any()
         p_local, sh2 = D.dist_project(None, w.geom, w.mu.astype(np.float64), project=project)
         # gather the forward stack to rank 0 for checking
         parts = [torch.zeros((len(AngleSharding(w.geom.n_angles, r, world).local_angles()),
