@@ -57,9 +57,13 @@ def _dist_worker(rank, world, port, out):
             xp64 = D.dist_backproject(tm, w.geom, y_local, precision="f64", plan=pl)
             pp, _ = D.dist_project(tm, w.geom, torch.from_numpy(w.mu).cuda(dev), plan=pl)
             torch.cuda.synchronize()
+        xs = D.dist_backproject(tm, w.geom, y_local, reduce="scatter")   # this rank's tet block
+        lo, hi = D.tet_shard(tm.n_tets, rank, world)
+        torch.cuda.synchronize()
         res = {"x": x.cpu().numpy(), "x64": x64.cpu().numpy(),
                "p": p_local.cpu().numpy(), "backend": dist.get_backend(),
-               "xp": xp.cpu().numpy(), "xp64": xp64.cpu().numpy(), "pp": pp.cpu().numpy()}
+               "xp": xp.cpu().numpy(), "xp64": xp64.cpu().numpy(), "pp": pp.cpu().numpy(),
+               "xs": xs.cpu().numpy(), "lo": lo, "hi": hi}
         np.savez(f"{out}.{rank}.npz", **res)
         dist.barrier()
     finally:
@@ -88,6 +92,9 @@ def test_two_rank_cuda_operators_match_oracle(tmp_path):
         np.testing.assert_array_equal(r["pp"], r["p"])
         np.testing.assert_allclose(r["xp"], r["x"], rtol=1e-6, atol=0)
         np.testing.assert_allclose(r["xp64"], r["x64"], rtol=1e-12, atol=0)
+        # reduce-scatter: the rank's block of the same reduced sum
+        lo, hi = int(r["lo"]), int(r["hi"])
+        np.testing.assert_allclose(r["xs"][: hi - lo], r["x"][lo:hi], rtol=1e-6, atol=0)
 
 
 def _cgls_worker(rank, world, port, out):
