@@ -8,16 +8,16 @@ north-star tolerances (tests/gpu_util.check_parity).  Prints one JSON line:
 cases, failures (seed + message), totals of rays, crossings and exact
 fallbacks.
 
-  python experiments/fuzz_campaign.py [first_seed] [n]
-  python experiments/fuzz_campaign.py mt first_seed n      # the paper's walk vs the MT oracle
-  python experiments/fuzz_campaign.py medium first_seed n  # 1e3-1e5-tet meshes
+  python tests/campaigns/fuzz_campaign.py [first_seed] [n]
+  python tests/campaigns/fuzz_campaign.py mt first_seed n      # the paper's walk vs the MT oracle
+  python tests/campaigns/fuzz_campaign.py medium first_seed n  # 1e3-1e5-tet meshes
 """
 import json
 import os
 import sys
 import traceback
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 from paper_1908_06909_b200 import tetproj as T  # noqa: E402

@@ -11,4 +11,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:trace_kernel -s 0 -c 3 -o gpurun_out/ev_ncu_c3 -f python bench.py --config c3 --no-cpu-baseline --e2e-steps 0 --steps 1 --warmup 3 > gpurun_out/ev_ncu_c3.log 2>&1; echo "ncu c3 $?"
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:trace_kernel -s 0 -c 1 -o gpurun_out/ev_ncu_c5_fwd -f python bench.py --config c5 --no-cpu-baseline --e2e-steps 0 --steps 1 --warmup 3 > gpurun_out/ev_ncu_c5_fwd.log 2>&1; echo "ncu c5 fwd $?"
 timeout 1500 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:trace_kernel<.bool.1' -s 0 -c 1 -o gpurun_out/ev_ncu_c5_back -f python bench.py --config c5 --no-cpu-baseline --e2e-steps 0 --steps 1 --warmup 3 > gpurun_out/ev_ncu_c5_back.log 2>&1; echo "ncu c5 back $?"
-timeout 1800 python experiments/fp_study.py > gpurun_out/fp_study.out 2>&1; echo "fp study $?"
+timeout 1800 python tests/campaigns/fp_study.py > gpurun_out/fp_study.out 2>&1; echo "fp study $?"
